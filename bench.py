@@ -1,0 +1,286 @@
+#!/usr/bin/env python
+"""AeroSketch update throughput on B200 (BASELINE.json metric: sketch update
+throughput, rows/s, at given d, eps; roofline fraction; CPU baseline beside).
+
+Workload (default): config C2 of BASELINE.json -- persistent (ATTP) stream,
+d=4096, eps=1/512 (ell=1024), low-rank-plus-noise generator k=256,
+sigma_j=0.99^j, noise 0.05, ||a||^2 log-uniform in [1,256]; fp64.
+A "step" = one update_block over `rows_per_step` consecutive rows of the
+stream. `value` = rows/s with inputs resident in HBM; `e2e` = the same through
+the public C-ABI with pinned host rows (H2D + event-log D2H inside the timed
+region). Multi-GPU: replicas only (one independent stream per GPU;
+DESIGN.md section 6).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(kind="attp", d=1024, eps=1 / 16, k=32, rho=0.9, noise=0.1, r_max=64.0, n=131072,
+               rows_per_step=16384, cpu_rows=4000,
+               name="C1 persistent stream n=131072 d=1024 eps=1/16 (k=32, sigma=0.9^j, noise 0.1, R=64)"),
+    "c2": dict(kind="attp", d=4096, eps=1 / 512, k=256, rho=0.99, noise=0.05, r_max=256.0, n=1048576,
+               rows_per_step=8192, cpu_rows=400,
+               name="C2 tight-eps persistent stream n=1048576 d=4096 eps=1/512 "
+                    "(k=256, sigma=0.99^j, noise 0.05, R=256)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--rows-per-step", type=int, default=0)
+    ap.add_argument("--cpu-rows", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self.stop_ev = index, [], threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop_ev.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop_ev.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def fp64_peak_tflops(torch, dev):
+    """Measured dense fp64 GEMM peak on this GPU (cuBLAS DGEMM 8192^3, best of
+    5): the roofline denominator for the fp64 products (MEASURED_PEAKS.json
+    carries only bf16 and HBM)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize(dev)
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    torch.cuda.empty_cache()
+    return best
+
+
+def cpu_oracle_rate(cfg, nrows, threads):
+    """Oracle restatement (oracle/) on the host cores over rows 1..nrows."""
+    from oracle import pyoracle as orc
+    import numpy as np
+    orc.set_threads(threads)
+    rows = orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, 0, 1, nrows)
+    s = orc.AttpState(cfg["d"], cfg["eps"], 1, 1000)
+    t0 = time.perf_counter()
+    s.update_block(rows, np.arange(1, nrows + 1))
+    dt = time.perf_counter() - t0
+    return nrows / dt, dt
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the reference path's CPU implementation (the oracle
+    port; the reference C++ needs Eigen, absent here) on all host threads."""
+    if rank != 0:
+        return
+    from oracle import pyoracle as orc
+    import numpy as np
+    threads = os.cpu_count() or 1
+    orc.set_threads(threads)
+    per = max(1, (args.cpu_rows or cfg["cpu_rows"]) // max(1, args.steps + args.warmup))
+    nrows = per * (args.steps + args.warmup)
+    rows = orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, 0, 1, nrows)
+    s = orc.AttpState(cfg["d"], cfg["eps"], 1, 1000)
+    for w in range(args.warmup):
+        s.update_block(rows[w * per:(w + 1) * per], np.arange(w * per + 1, (w + 1) * per + 1))
+    t0 = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        s.update_block(rows[k * per:(k + 1) * per], np.arange(k * per + 1, (k + 1) * per + 1))
+    dt = time.perf_counter() - t0
+    v = per * args.steps / dt
+    sample = f"rows {args.warmup * per + 1}..{nrows} of the {args.config.upper()} stream (from an empty sketch)"
+    print(json.dumps({
+        "impl": "reference", "metric": "sketch update throughput", "value": v, "unit": "rows/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "rows_per_step": per},
+        "cpu_baseline": {"value": v, "unit": "rows/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    import numpy as np
+    import torch
+    import paper_2601_02019_b200 as prod
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    S = args.rows_per_step or cfg["rows_per_step"]
+    steps, warm = args.steps, args.warmup
+    nrows = S * (steps + warm)
+    d = cfg["d"]
+    rows = torch.empty((nrows, d), dtype=torch.float64, device=dev)
+    prod.gen_rows_device(rows, 1, d, cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1 + rank,
+                         stream=0, device=local)
+    torch.cuda.synchronize(dev)
+    ts_all = np.arange(1, nrows + 1, dtype=np.int64)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def run(sk, host_rows=None):
+        for w in range(warm):
+            sl = slice(w * S, (w + 1) * S)
+            sk.update_block(rows[sl] if host_rows is None else host_rows[sl], ts_all[sl])
+        sk.synchronize()
+        sk.reset_profile()
+        ext = torch.cuda.ExternalStream(sk.stream_handle(), device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        l0 = prod.kernel_launches()
+        evs = []
+        with ClockSampler(local) as clk:
+            e0.record(ext)
+            for k in range(warm, warm + steps):
+                sl = slice(k * S, (k + 1) * S)
+                evs.append(sk.update_block(rows[sl] if host_rows is None else host_rows[sl], ts_all[sl]))
+            e1.record(ext)
+            e1.synchronize()
+        launches = prod.kernel_launches() - l0
+        ms = e0.elapsed_time(e1)
+        barrier()
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches, clk.summary(), np.concatenate(evs)
+
+    sk = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, profile=True)
+    ms, launches, clocks, ev = run(sk)
+    prof = sk.profile()
+    info = sk.info()
+    value = world * S * steps / (ms * 1e-3)
+
+    e2e = None
+    if not args.no_e2e:
+        host = rows.cpu().pin_memory().numpy()
+        sk2 = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local)
+        ms2, _, _, _ = run(sk2, host_rows=host)
+        e2e = {"value": world * S * steps / (ms2 * 1e-3), "unit": "rows/s",
+               "h2d_bytes_per_step": S * d * 8, "d2h_bytes_per_step": S * ev.dtype.itemsize}
+        del sk2, host
+
+    out = None
+    if rank == 0:
+        peak = fp64_peak_tflops(torch, dev)
+        achieved = (prof["product_flops"] / max(prof["product_ms"], 1e-9)) / 1e9  # TFLOP/s
+        traffic = None
+        summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        if os.path.exists(summ):
+            try:
+                traffic = json.load(open(summ)).get("product_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
+                    "kernel": "k_dgemm (batched masked G.X power/subspace-iteration product)",
+                    "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 fp64 (not in MEASURED_PEAKS.json)",
+                    "product_share_of_step": prof["product_ms"] / ms,
+                    "flops_per_launch": prof["product_flops"] / max(1, prof["product_launches"]),
+                    "ms_per_launch": prof["product_ms"] / max(1, prof["product_launches"])}
+        cpu = None
+        if not args.no_cpu:
+            threads = 1
+            n_cpu = args.cpu_rows or cfg["cpu_rows"]
+            rate, dt = cpu_oracle_rate(cfg, n_cpu, threads)
+            cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
+                   "sample": f"rows 1..{n_cpu} of the {args.config.upper()} stream from an empty sketch "
+                             f"({dt:.1f} s; oracle restatement over OpenBLAS, 1 thread like the reference)"}
+        out = {
+            "metric": "sketch update throughput", "value": value, "unit": "rows/s", "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "rows_per_step": S, "d": d, "eps": cfg["eps"],
+                       "ell": info.ell, "timed_rows": f"{warm * S + 1}..{nrows}",
+                       "l2": f"inputs larger than L2 ({S * d * 8 / 2**20:.0f} MiB per step)",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks,
+            "stats": {"gate_fire_rate": float(ev["gate_fired"].mean()), "dump_rate": float(ev["dumped"].mean()),
+                      "reduces": int(ev["reduced"].sum()), "batches": int(info.device_batches),
+                      "mispredicts": int(info.device_mispredicts), "snap_cols": int(info.snap_cols),
+                      "iterate_ms": prof["iterate_ms"], "reduce_ms": prof["reduce_ms"],
+                      "product_ms": prof["product_ms"], "product_launches": int(prof["product_launches"])},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

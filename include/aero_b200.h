@@ -1,0 +1,219 @@
+/*
+ * aero_b200.h -- C-ABI of the B200-native AeroSketch update path.
+ *
+ * Drop-in boundary for the reference C++ sketch API (arXiv 2601.02019,
+ * /root/reference/proj/include/aero). The reference has no FFI layer of its
+ * own; each entry point below replaces one reference member function, cited
+ * as file:line. All pointers are HOST pointers unless the name ends in
+ * _device. Matrices are row-major with an explicit leading dimension.
+ * Every call returns a status code (0 = ok) mirroring the reference's
+ * exception taxonomy (errors.hpp:15-33); aero_last_error() gives the text.
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns AERO_CUDA_ERROR.
+ */
+#ifndef AERO_B200_H
+#define AERO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.hpp:15-33) */
+#define AERO_OK 0
+#define AERO_INVALID_INPUT 1        /* aero::InvalidInput  */
+#define AERO_FORMAT_ERROR 2         /* aero::FormatError   */
+#define AERO_PROTOCOL_ERROR 3       /* aero::ProtocolError */
+#define AERO_ORACLE_CAP_EXCEEDED 4  /* aero::OracleCapExceeded */
+#define AERO_CUDA_ERROR 10
+#define AERO_INTERNAL_ERROR 11
+
+/* threshold modes */
+#define AERO_THETA_FIXED 0  /* AeroState: theta set by aero_set_theta / per-row array */
+#define AERO_THETA_ATTP 1   /* AttpState (attp.hpp:21-26): theta = eps * running ||A||_F^2 */
+
+/* flags */
+#define AERO_FLAG_EXACT 1   /* no speculative row batching (one row per device step) */
+#define AERO_FLAG_PROFILE 2 /* time the batched G.X products with CUDA events */
+
+typedef struct aero_sketch aero_sketch; /* opaque AeroState / AttpState */
+
+typedef struct aero_cfg {
+    int32_t d;          /* row dimension (sketch.cpp:22-31) */
+    int32_t ell;        /* 0: ell = ceil(2/eps) (sketch.cpp:30) */
+    double eps;         /* (0, 1] */
+    double theta;       /* initial threshold >= 0 */
+    double eps_si;      /* simul_iter accuracy; 0 -> 0.4 (sketch.cpp:23) */
+    uint64_t seed;      /* RngState(seed, stream) of the sketch (rng.hpp:45-48) */
+    uint64_t stream;
+    int32_t device;     /* CUDA device ordinal */
+    int32_t theta_mode; /* AERO_THETA_FIXED or AERO_THETA_ATTP */
+    int32_t flags;      /* AERO_FLAG_* */
+    int32_t max_batch;  /* speculative batch rows (0 = auto) */
+} aero_cfg;
+
+/* per-row event record (UpdateStats, sketch.hpp:33-39, plus the trace the
+ * parity tests compare); same layout as the oracle's Event */
+typedef struct aero_event {
+    int64_t t;
+    int64_t forks_before, forks_after;
+    int32_t rows_after, reduced, gate_fired, dumped;
+    int32_t doubling_steps, simul_calls, xi, k_last;
+    double theta, sigma1_sq, tail_sq;
+} aero_event;
+
+typedef struct aero_info {
+    int32_t d, ell, rows;       /* rows = residual buffer rows */
+    int64_t clock, last_dump_t; /* sketch.hpp:74,86 */
+    int64_t forks;              /* RngState fork counter */
+    int64_t snaps;              /* snapshot queue length */
+    int64_t snap_cols;          /* sum of snapshot widths (xi) in the queue */
+    double theta, fro_mass;     /* fro_mass: AttpState::fro_mass (attp.hpp:34) */
+    int64_t device_rows_processed, device_batches, device_mispredicts;
+} aero_info;
+
+/* ---- AeroState / AttpState --------------------------------------------- */
+/* AeroState(d, eps, theta, rng) (sketch.cpp:22-31); AttpState(d, eps, rng)
+ * when theta_mode == AERO_THETA_ATTP (attp.hpp:17-19) */
+int aero_create(const aero_cfg* cfg, aero_sketch** out);
+int aero_destroy(aero_sketch* h);
+/* AeroState::set_theta (sketch.cpp:33-36) */
+int aero_set_theta(aero_sketch* h, double theta);
+/* n sequential AeroState::update / AttpState::update calls (sketch.cpp:82-141,
+ * attp.hpp:21-26). t: n strictly increasing timestamps > clock. theta_per_row
+ * (nullable, fixed mode only) sets the threshold before each row. log_out
+ * (nullable) receives one aero_event per row. */
+int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
+                      const double* theta_per_row, aero_event* log_out);
+/* same, rows already resident in device memory (ld in elements) */
+int aero_update_block_device(aero_sketch* h, const double* rows_device, int64_t n, int64_t ld,
+                             const int64_t* t, const double* theta_per_row, aero_event* log_out);
+/* AeroState::query(lb, ub) (sketch.cpp:143-160): ell x d row-major */
+int aero_query(aero_sketch* h, int64_t lb, int64_t ub, double* out_ell_by_d);
+/* the restored Gram before the final shrink (d x d row-major, symmetric) */
+int aero_query_gram(aero_sketch* h, int64_t lb, int64_t ub, double* out_d_by_d);
+/* AeroState::residual() (sketch.hpp:77): rows x d row-major */
+int aero_residual(aero_sketch* h, double* out, int64_t max_rows);
+/* snapshot queue access (sketch.hpp:78-79; callers pop it: sliding_window.cpp:59-65,
+ * distributed.cpp:74-77). z: d x xi row-major, m: xi x d row-major (nullable). */
+int aero_snap_count(aero_sketch* h, int64_t* count);
+int aero_snap_info(aero_sketch* h, int64_t idx, int32_t* xi, int64_t* s, int64_t* t, double* theta);
+int aero_snap_get(aero_sketch* h, int64_t idx, double* z, double* m);
+int aero_snap_pop_front(aero_sketch* h);
+/* AeroState::last_update_stats (sketch.hpp:80) as an event record */
+int aero_last_stats(aero_sketch* h, aero_event* out);
+int aero_get_info(aero_sketch* h, aero_info* out);
+/* wait for all device work of this sketch */
+int aero_synchronize(aero_sketch* h);
+/* the cudaStream_t this sketch launches its kernels on */
+void* aero_stream(aero_sketch* h);
+/* AERO_FLAG_PROFILE: CUDA-event time, launches, useful flops (sum over the
+ * active job columns of 2 r_j^2 k_j) and compulsory bytes of the batched
+ * power/subspace-iteration products (the dominant kernel), plus batch counts */
+typedef struct aero_profile {
+    double product_ms;
+    int64_t product_launches;
+    double product_flops, product_bytes;
+    double iterate_ms;   /* init + products + normalizations */
+    double reduce_ms;    /* FD reduce (eigensolver + rotation) */
+    int64_t reduces;
+} aero_profile;
+int aero_get_profile(aero_sketch* h, aero_profile* out);
+int aero_reset_profile(aero_sketch* h);
+
+/* ---- AttpState::query(t) (attp.hpp:29-32): prefix sketch at time t ---- */
+int aero_attp_query(aero_sketch* h, int64_t t, double* out_ell_by_d);
+
+/* ---- MlState: sliding-window multi-level sketch
+ * (sliding_window.hpp:39-81, sliding_window.cpp:15-156) ---------------- */
+typedef struct aero_ml aero_ml;
+typedef struct aero_ml_query_result {
+    int32_t level, fallback, heavy_used, _pad;
+    int64_t xi_sum;
+} aero_ml_query_result;
+typedef struct aero_ml_info {
+    int32_t d, ell, levels, _pad;
+    int64_t n, cap, clock, norm_warnings, stored_floats;
+    double window_mass;
+} aero_ml_info;
+int aero_ml_create(int32_t d, int64_t window, double r_max, double eps, uint64_t seed,
+                   uint64_t stream, int32_t device, aero_ml** out);
+int aero_ml_destroy(aero_ml* h);
+int aero_ml_update_block(aero_ml* h, const double* rows, int64_t n, int64_t ld, const int64_t* t);
+int aero_ml_update_block_device(aero_ml* h, const double* rows_device, int64_t n, int64_t ld,
+                                const int64_t* t);
+int aero_ml_query(aero_ml* h, double* out_ell_by_d, aero_ml_query_result* res);
+int aero_ml_get_info(aero_ml* h, aero_ml_info* out);
+double aero_ml_theta(aero_ml* h, int32_t level);
+/* level j's AeroState (borrowed handle, owned by the MlState) */
+aero_sketch* aero_ml_level(aero_ml* h, int32_t level);
+int aero_ml_heavy_count(aero_ml* h, int32_t level, int64_t* count);
+int aero_ml_heavy_get(aero_ml* h, int32_t level, int64_t idx, double* row, int64_t* s, int64_t* t);
+
+/* ---- distributed: site -> coordinator merge (distributed.hpp:23-135,
+ * distributed.cpp:16-269), one site per GPU ------------------------------ */
+/* Norm-only replay of the FroMass / broadcast protocol (distributed.cpp:31-69,
+ * 107-123, 201-239): given every site's squared row norms (m x T, row-major),
+ * returns each site's threshold per tick (m x T) and the protocol byte count
+ * of the mass messages and broadcasts. Pure host integer/fp64 logic. */
+int aero_dist_theta_schedule(int32_t m, int64_t T, double eps, int64_t latency,
+                             const double* sq_norms, double* theta_out, int64_t* mass_bytes,
+                             int64_t* broadcasts);
+typedef struct aero_coord aero_coord;
+/* coordinator accumulator B (d x d fp64) on `device`; nccl_comm is an
+ * ncclComm_t (or NULL for single-process use) */
+int aero_coord_create(int32_t d, int32_t m, int32_t device, void* nccl_comm, aero_coord** out);
+int aero_coord_destroy(aero_coord* h);
+/* CoordinatorState::receive(SnapshotUpdate) for every snapshot queued in the
+ * site sketch (distributed.cpp:124-136), popping them (distributed.cpp:74-77);
+ * returns the protocol bytes 8*(d*xi + xi*d) + 16 per message */
+int aero_coord_absorb_snapshots(aero_coord* h, aero_sketch* site, int64_t* bytes);
+/* probe_gram (distributed.cpp:159-173): this rank's absorbed contributions
+ * plus the residual Grams of its `nsites` site sketches, summed over ranks with
+ * ncclReduce to `root`; on root, shrink_to_sketch(B, ell) -> out (ell x d
+ * row-major, nullable) and the d x d Gram (nullable) */
+int aero_coord_probe(aero_coord* h, aero_sketch* const* sites, int32_t nsites, int32_t root,
+                     int32_t ell, double* out_ell_by_d, double* out_gram);
+/* NCCL helpers so callers need no NCCL headers: 128-byte unique id */
+int aero_nccl_get_unique_id(char* id128);
+int aero_nccl_comm_init(const char* id128, int32_t nranks, int32_t rank, int32_t device,
+                        void** comm_out);
+int aero_nccl_comm_destroy(void* comm);
+
+/* ---- CodState: sliding-window AMM (amm.hpp:35-69, amm.cpp:27-122) ----- */
+typedef struct aero_cod aero_cod;
+int aero_cod_create(int32_t dx, int32_t dy, double eps, double theta, int64_t window,
+                    uint64_t seed, uint64_t stream, int32_t device, aero_cod** out);
+int aero_cod_destroy(aero_cod* h);
+int aero_cod_update_block(aero_cod* h, const double* xs, const double* ys, int64_t n,
+                          const int64_t* t, aero_event* log_out);
+/* CodState::query: a* (dx x ell) and b* (dy x ell), row-major */
+int aero_cod_query(aero_cod* h, double* astar, double* bstar);
+int aero_cod_query_product(aero_cod* h, double* p_dx_by_dy);
+int aero_cod_info(aero_cod* h, int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock);
+
+/* ---- stream generators (BASELINE.json configs; DESIGN.md GENERATOR spec) */
+typedef struct aero_gen_params {
+    int32_t d, k, k2, _pad;
+    double rho, noise, r_max, rho2, scale2;
+    uint64_t seed, stream, basis_stream;
+    int64_t drift_period;
+} aero_gen_params;
+/* rows t0 .. t0+n-1 into device memory (n x d row-major) */
+int aero_gen_rows_device(const aero_gen_params* p, int64_t t0, int64_t n, double* out_device,
+                         int32_t device);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char* aero_last_error(void);  /* thread-local text of the last failure */
+const char* aero_version(void);
+/* device kernels launched by this library so far (all handles, this process) */
+int64_t aero_kernel_launches(void);
+/* RngState draws on the device (test hook): count gaussians of fork #fork of
+ * RngState(seed, stream) (fork 0 = the root), to host memory */
+int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AERO_B200_H */

@@ -1,0 +1,501 @@
+"""ctypes binding of libaero_b200.so (include/aero_b200.h).
+
+Host-side mirror of the reference C++ sketch API (/root/reference/proj/include/
+aero/*.hpp): AeroState, AttpState, MlState, the distributed site/coordinator
+merge, and the stream generator. Every compute call goes through the C-ABI to
+the sm_100a kernels; there is no CPU fallback -- on a machine without a CUDA
+device the constructors raise CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libaero_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "aero_b200.h")
+
+i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+vp = C.c_void_p
+P = C.POINTER
+
+AERO_THETA_FIXED, AERO_THETA_ATTP = 0, 1
+AERO_FLAG_EXACT = 1
+AERO_FLAG_PROFILE = 2
+
+
+class InvalidInput(ValueError):
+    pass
+
+
+class FormatError(RuntimeError):
+    pass
+
+
+class ProtocolError(RuntimeError):
+    pass
+
+
+class OracleCapExceeded(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRS = {1: InvalidInput, 2: FormatError, 3: ProtocolError, 4: OracleCapExceeded, 10: CudaError}
+
+
+class Cfg(C.Structure):
+    _fields_ = [("d", i32), ("ell", i32), ("eps", f64), ("theta", f64), ("eps_si", f64),
+                ("seed", u64), ("stream", u64), ("device", i32), ("theta_mode", i32),
+                ("flags", i32), ("max_batch", i32)]
+
+
+class Event(C.Structure):
+    _fields_ = [("t", i64), ("forks_before", i64), ("forks_after", i64),
+                ("rows_after", C.c_int32), ("reduced", C.c_int32), ("gate_fired", C.c_int32),
+                ("dumped", C.c_int32), ("doubling_steps", C.c_int32), ("simul_calls", C.c_int32),
+                ("xi", C.c_int32), ("k_last", C.c_int32),
+                ("theta", f64), ("sigma1_sq", f64), ("tail_sq", f64)]
+
+
+EVENT_DTYPE = np.dtype([
+    ("t", "<i8"), ("forks_before", "<i8"), ("forks_after", "<i8"),
+    ("rows_after", "<i4"), ("reduced", "<i4"), ("gate_fired", "<i4"), ("dumped", "<i4"),
+    ("doubling_steps", "<i4"), ("simul_calls", "<i4"), ("xi", "<i4"), ("k_last", "<i4"),
+    ("theta", "<f8"), ("sigma1_sq", "<f8"), ("tail_sq", "<f8"),
+])
+assert EVENT_DTYPE.itemsize == C.sizeof(Event)
+
+
+class Info(C.Structure):
+    _fields_ = [("d", i32), ("ell", i32), ("rows", i32), ("clock", i64), ("last_dump_t", i64),
+                ("forks", i64), ("snaps", i64), ("snap_cols", i64), ("theta", f64),
+                ("fro_mass", f64), ("device_rows_processed", i64), ("device_batches", i64),
+                ("device_mispredicts", i64)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("product_ms", f64), ("product_launches", i64), ("product_flops", f64),
+                ("product_bytes", f64), ("iterate_ms", f64), ("reduce_ms", f64), ("reduces", i64)]
+
+
+class MlQueryResult(C.Structure):
+    _fields_ = [("level", i32), ("fallback", i32), ("heavy_used", i32), ("_pad", i32),
+                ("xi_sum", i64)]
+
+
+class MlInfo(C.Structure):
+    _fields_ = [("d", i32), ("ell", i32), ("levels", i32), ("_pad", i32), ("n", i64), ("cap", i64),
+                ("clock", i64), ("norm_warnings", i64), ("stored_floats", i64),
+                ("window_mass", f64)]
+
+
+class GenParams(C.Structure):
+    _fields_ = [("d", i32), ("k", i32), ("k2", i32), ("_pad", i32), ("rho", f64), ("noise", f64),
+                ("r_max", f64), ("rho2", f64), ("scale2", f64), ("seed", u64), ("stream", u64),
+                ("basis_stream", u64), ("drift_period", i64)]
+
+
+# every entry point declared in include/aero_b200.h: (name, restype, argtypes)
+SIGNATURES = [
+    ("aero_create", i32, [P(Cfg), P(vp)]),
+    ("aero_destroy", i32, [vp]),
+    ("aero_set_theta", i32, [vp, f64]),
+    ("aero_update_block", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
+    ("aero_update_block_device", i32, [vp, vp, i64, i64, P(i64), P(f64), P(Event)]),
+    ("aero_query", i32, [vp, i64, i64, P(f64)]),
+    ("aero_query_gram", i32, [vp, i64, i64, P(f64)]),
+    ("aero_residual", i32, [vp, P(f64), i64]),
+    ("aero_snap_count", i32, [vp, P(i64)]),
+    ("aero_snap_info", i32, [vp, i64, P(i32), P(i64), P(i64), P(f64)]),
+    ("aero_snap_get", i32, [vp, i64, P(f64), P(f64)]),
+    ("aero_snap_pop_front", i32, [vp]),
+    ("aero_last_stats", i32, [vp, P(Event)]),
+    ("aero_get_info", i32, [vp, P(Info)]),
+    ("aero_synchronize", i32, [vp]),
+    ("aero_attp_query", i32, [vp, i64, P(f64)]),
+    ("aero_stream", vp, [vp]),
+    ("aero_get_profile", i32, [vp, P(Profile)]),
+    ("aero_reset_profile", i32, [vp]),
+    ("aero_ml_create", i32, [i32, i64, f64, f64, u64, u64, i32, P(vp)]),
+    ("aero_ml_destroy", i32, [vp]),
+    ("aero_ml_update_block", i32, [vp, P(f64), i64, i64, P(i64)]),
+    ("aero_ml_update_block_device", i32, [vp, vp, i64, i64, P(i64)]),
+    ("aero_ml_query", i32, [vp, P(f64), P(MlQueryResult)]),
+    ("aero_ml_get_info", i32, [vp, P(MlInfo)]),
+    ("aero_ml_theta", f64, [vp, i32]),
+    ("aero_ml_level", vp, [vp, i32]),
+    ("aero_ml_heavy_count", i32, [vp, i32, P(i64)]),
+    ("aero_ml_heavy_get", i32, [vp, i32, i64, P(f64), P(i64), P(i64)]),
+    ("aero_dist_theta_schedule", i32, [i32, i64, f64, i64, P(f64), P(f64), P(i64), P(i64)]),
+    ("aero_coord_create", i32, [i32, i32, i32, vp, P(vp)]),
+    ("aero_coord_destroy", i32, [vp]),
+    ("aero_coord_absorb_snapshots", i32, [vp, vp, P(i64)]),
+    ("aero_coord_probe", i32, [vp, P(vp), i32, i32, i32, P(f64), P(f64)]),
+    ("aero_nccl_get_unique_id", i32, [C.c_char_p]),
+    ("aero_nccl_comm_init", i32, [C.c_char_p, i32, i32, i32, P(vp)]),
+    ("aero_nccl_comm_destroy", i32, [vp]),
+    ("aero_cod_create", i32, [i32, i32, f64, f64, i64, u64, u64, i32, P(vp)]),
+    ("aero_cod_destroy", i32, [vp]),
+    ("aero_cod_update_block", i32, [vp, P(f64), P(f64), i64, P(i64), P(Event)]),
+    ("aero_cod_query", i32, [vp, P(f64), P(f64)]),
+    ("aero_cod_query_product", i32, [vp, P(f64)]),
+    ("aero_cod_info", i32, [vp, P(i32), P(i64), P(i64), P(i64)]),
+    ("aero_gen_rows_device", i32, [P(GenParams), i64, i64, vp, i32]),
+    ("aero_last_error", C.c_char_p, []),
+    ("aero_version", C.c_char_p, []),
+    ("aero_kernel_launches", i64, []),
+    ("aero_rng_gaussians", i32, [u64, u64, i64, i64, P(f64)]),
+]
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree extension; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _chk(rc):
+    if rc != 0:
+        raise _ERRS.get(rc, RuntimeError)(lib().aero_last_error().decode())
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dp(a):
+    return a.ctypes.data_as(P(f64)) if a is not None else None
+
+
+def _lp(a):
+    return a.ctypes.data_as(P(i64))
+
+
+def kernel_launches() -> int:
+    return int(lib().aero_kernel_launches())
+
+
+def rng_gaussians(seed, stream, fork, count):
+    out = np.empty(count)
+    _chk(lib().aero_rng_gaussians(seed, stream, fork, count, _dp(out)))
+    return out
+
+
+def _device_ptr(x):
+    """(pointer, ld) of a CUDA torch tensor of shape (n, d), float64."""
+    import torch
+    assert x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.stride(1) == 1
+    return C.c_void_p(x.data_ptr()), x.stride(0)
+
+
+class AeroState:
+    """reference AeroState (sketch.hpp:42-99): construct with d and eps (or an
+    explicit ell), update by row or row block, query(lb, ub)."""
+
+    def __init__(self, d, eps, theta=0.0, seed=0, stream=0, device=0, ell=0, theta_mode=AERO_THETA_FIXED,
+                 exact=False, max_batch=0, profile=False, _handle=None, _owner=None):
+        self._owner = _owner
+        if _handle is not None:
+            self._h, self._own = _handle, False
+        else:
+            cfg = Cfg(d=d, ell=ell, eps=eps, theta=theta, eps_si=0.0, seed=seed, stream=stream,
+                      device=device, theta_mode=theta_mode,
+                      flags=(AERO_FLAG_EXACT if exact else 0) | (AERO_FLAG_PROFILE if profile else 0),
+                      max_batch=max_batch)
+            h = vp()
+            _chk(lib().aero_create(C.byref(cfg), C.byref(h)))
+            self._h, self._own = h, True
+        inf = self.info()
+        self.d, self.ell = inf.d, inf.ell
+
+    def close(self):
+        if getattr(self, "_own", False) and self._h:
+            lib().aero_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        inf = Info()
+        _chk(lib().aero_get_info(self._h, C.byref(inf)))
+        return inf
+
+    @property
+    def clock(self):
+        return self.info().clock
+
+    @property
+    def theta(self):
+        return self.info().theta
+
+    @property
+    def forks(self):
+        return self.info().forks
+
+    @property
+    def last_dump_time(self):
+        return self.info().last_dump_t
+
+    def set_theta(self, theta):
+        _chk(lib().aero_set_theta(self._h, theta))
+
+    def update_block(self, rows, ts, thetas=None):
+        """n sequential updates (sketch.cpp:82-141); returns the event log."""
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = ts.shape[0]
+        ev = (Event * max(n, 1))()
+        th = _f64(thetas) if thetas is not None else None
+        if hasattr(rows, "is_cuda") and rows.is_cuda:
+            ptr, ld = _device_ptr(rows)
+            if rows.shape[1] != self.d:
+                raise InvalidInput("AeroState: row dimension mismatch")
+            _chk(lib().aero_update_block_device(self._h, ptr, n, ld, _lp(ts), _dp(th), ev))
+        else:
+            rows = _f64(rows)
+            if rows.ndim != 2 or rows.shape[1] != self.d:
+                raise InvalidInput("AeroState: row dimension mismatch")
+            _chk(lib().aero_update_block(self._h, _dp(rows), n, self.d, _lp(ts), _dp(th), ev))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
+
+    def update(self, a, i):
+        return self.update_block(np.asarray(a, np.float64)[None, :], [i])[0]
+
+    def query(self, lb, ub):
+        out = np.empty((self.ell, self.d))
+        _chk(lib().aero_query(self._h, lb, ub, _dp(out)))
+        return out
+
+    def query_gram(self, lb, ub):
+        out = np.empty((self.d, self.d))
+        _chk(lib().aero_query_gram(self._h, lb, ub, _dp(out)))
+        return out
+
+    def residual(self):
+        r = self.info().rows
+        out = np.empty((r, self.d))
+        _chk(lib().aero_residual(self._h, _dp(out), r))
+        return out
+
+    def snap_count(self):
+        n = i64()
+        _chk(lib().aero_snap_count(self._h, C.byref(n)))
+        return n.value
+
+    def snaps(self):
+        out = []
+        for idx in range(self.snap_count()):
+            xi, s, t, th = i32(), i64(), i64(), f64()
+            _chk(lib().aero_snap_info(self._h, idx, C.byref(xi), C.byref(s), C.byref(t), C.byref(th)))
+            z, m = np.empty((self.d, xi.value)), np.empty((xi.value, self.d))
+            _chk(lib().aero_snap_get(self._h, idx, _dp(z), _dp(m)))
+            out.append(dict(z=z, m=m, s=s.value, t=t.value, theta=th.value))
+        return out
+
+    def snap_meta(self):
+        out = []
+        for idx in range(self.snap_count()):
+            xi, s, t, th = i32(), i64(), i64(), f64()
+            _chk(lib().aero_snap_info(self._h, idx, C.byref(xi), C.byref(s), C.byref(t), C.byref(th)))
+            out.append((xi.value, s.value, t.value, th.value))
+        return out
+
+    def snap_pop_front(self):
+        _chk(lib().aero_snap_pop_front(self._h))
+
+    def last_update_stats(self):
+        ev = Event()
+        _chk(lib().aero_last_stats(self._h, C.byref(ev)))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=1)[0]
+
+    def synchronize(self):
+        _chk(lib().aero_synchronize(self._h))
+
+    def stream_handle(self) -> int:
+        return int(lib().aero_stream(self._h) or 0)
+
+    def profile(self):
+        p = Profile()
+        _chk(lib().aero_get_profile(self._h, C.byref(p)))
+        return {f: getattr(p, f) for f, _ in Profile._fields_}
+
+    def reset_profile(self):
+        _chk(lib().aero_reset_profile(self._h))
+
+
+class AttpState(AeroState):
+    """reference AttpState (attp.hpp:15-43): theta = eps * running mass."""
+
+    def __init__(self, d, eps, seed=0, stream=0, device=0, exact=False, max_batch=0, profile=False):
+        super().__init__(d, eps, 0.0, seed, stream, device, theta_mode=AERO_THETA_ATTP,
+                         exact=exact, max_batch=max_batch, profile=profile)
+
+    @property
+    def inner(self):
+        return self
+
+    @property
+    def fro_mass(self):
+        return self.info().fro_mass
+
+    def query(self, t, ub=None):  # AttpState::query(t); AeroState::query(lb, ub) if ub given
+        if ub is not None:
+            return AeroState.query(self, t, ub)
+        out = np.empty((self.ell, self.d))
+        _chk(lib().aero_attp_query(self._h, t, _dp(out)))
+        return out
+
+
+class MlState:
+    """reference MlState (sliding_window.hpp:39-81)."""
+
+    def __init__(self, d, n, r_max, eps, seed=0, stream=0, device=0):
+        h = vp()
+        _chk(lib().aero_ml_create(d, n, r_max, eps, seed, stream, device, C.byref(h)))
+        self._h, self.d, self.n = h, d, n
+        inf = self.info()
+        self.levels, self.ell = inf.levels, inf.ell
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_ml_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        inf = MlInfo()
+        _chk(lib().aero_ml_get_info(self._h, C.byref(inf)))
+        return inf
+
+    def theta(self, j):
+        return lib().aero_ml_theta(self._h, j)
+
+    def update_block(self, rows, ts):
+        ts = np.ascontiguousarray(ts, np.int64)
+        if hasattr(rows, "is_cuda") and rows.is_cuda:
+            ptr, ld = _device_ptr(rows)
+            _chk(lib().aero_ml_update_block_device(self._h, ptr, ts.shape[0], ld, _lp(ts)))
+        else:
+            rows = _f64(rows)
+            if rows.ndim != 2 or rows.shape[1] != self.d:
+                raise InvalidInput("MlState: row dimension mismatch")
+            _chk(lib().aero_ml_update_block(self._h, _dp(rows), rows.shape[0], self.d, _lp(ts)))
+
+    def update(self, a, i):
+        self.update_block(np.asarray(a, np.float64)[None, :], [i])
+
+    def query(self):
+        sk = np.empty((self.ell, self.d))
+        r = MlQueryResult()
+        _chk(lib().aero_ml_query(self._h, _dp(sk), C.byref(r)))
+        return dict(sketch=sk, level=r.level, fallback=bool(r.fallback), xi_sum=r.xi_sum,
+                    heavy_used=r.heavy_used)
+
+    def level_state(self, j):
+        h = lib().aero_ml_level(self._h, j)
+        if not h:
+            raise InvalidInput("MlState: level out of range")
+        return AeroState(0, 0, _handle=vp(h), _owner=self)
+
+    def heavy_count(self, j):
+        n = i64()
+        _chk(lib().aero_ml_heavy_count(self._h, j, C.byref(n)))
+        return n.value
+
+    def heavy(self, j):
+        out = []
+        for idx in range(self.heavy_count(j)):
+            row, s, t = np.empty(self.d), i64(), i64()
+            _chk(lib().aero_ml_heavy_get(self._h, j, idx, _dp(row), C.byref(s), C.byref(t)))
+            out.append(dict(row=row, s=s.value, t=t.value))
+        return out
+
+
+def dist_theta_schedule(sq_norms, eps, latency=0):
+    """Per-site thresholds from the norm-only protocol replay
+    (distributed.cpp:31-69,107-123,201-239). sq_norms: (m, T)."""
+    sq = _f64(sq_norms)
+    m, T = sq.shape
+    th = np.empty_like(sq)
+    mb, bc = i64(), i64()
+    _chk(lib().aero_dist_theta_schedule(m, T, eps, latency, _dp(sq), _dp(th), C.byref(mb), C.byref(bc)))
+    return th, mb.value, bc.value
+
+
+class Coordinator:
+    """reference CoordinatorState (distributed.hpp:78-105) as a device
+    accumulator per rank, merged with ncclReduce at probe time."""
+
+    def __init__(self, d, m, device=0, nccl_comm=None):
+        h = vp()
+        _chk(lib().aero_coord_create(d, m, device, nccl_comm, C.byref(h)))
+        self._h, self.d = h, d
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_coord_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def absorb(self, site: AeroState) -> int:
+        b = i64()
+        _chk(lib().aero_coord_absorb_snapshots(self._h, site._h, C.byref(b)))
+        return b.value
+
+    def probe(self, sites, ell, root=0, want_gram=False):
+        arr = (vp * max(len(sites), 1))(*[s._h for s in sites])
+        out = np.empty((ell, self.d))
+        gram = np.empty((self.d, self.d)) if want_gram else None
+        _chk(lib().aero_coord_probe(self._h, arr, len(sites), root, ell, _dp(out), _dp(gram)))
+        return out, gram
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _chk(lib().aero_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, nranks, rank, device):
+    c = vp()
+    _chk(lib().aero_nccl_comm_init(uid, nranks, rank, device, C.byref(c)))
+    return c
+
+
+def gen_rows_device(out, t0, d, k, rho, noise, r_max, seed, stream=0, drift=0, k2=0, rho2=0.9,
+                    scale2=0.5, basis_stream=0, device=0):
+    """Fill a CUDA float64 tensor (n, d) with rows t0..t0+n-1 of the config
+    generator (DESIGN.md GENERATOR spec)."""
+    p = GenParams(d=d, k=k, k2=k2, rho=rho, noise=noise, r_max=r_max, rho2=rho2, scale2=scale2,
+                  seed=seed, stream=stream, basis_stream=basis_stream, drift_period=drift)
+    _chk(lib().aero_gen_rows_device(C.byref(p), t0, out.shape[0], C.c_void_p(out.data_ptr()), device))

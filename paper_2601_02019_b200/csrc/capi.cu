@@ -1,0 +1,363 @@
+// extern "C" boundary (include/aero_b200.h): maps the reference's exceptions
+// (errors.hpp:15-33) to status codes; no torch types cross this line.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "aero_common.cuh"
+#include "engines.hpp"
+#include "sketch.hpp"
+
+using namespace aero_b200;
+
+struct aero_sketch {
+    Sketch* s;
+    bool owned;
+};
+
+namespace aero_b200 {
+long long launches_total();
+thread_local std::string g_last_error;
+}  // namespace aero_b200
+
+namespace {
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return AERO_OK;
+    } catch (const InvalidInput& e) {
+        g_last_error = e.what();
+        return AERO_INVALID_INPUT;
+    } catch (const ProtocolError& e) {
+        g_last_error = e.what();
+        return AERO_PROTOCOL_ERROR;
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return AERO_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return AERO_INTERNAL_ERROR;
+    }
+}
+int require(const void* p, const char* what) {
+    if (!p) {
+        g_last_error = std::string(what) + ": null handle";
+        return AERO_INVALID_INPUT;
+    }
+    return AERO_OK;
+}
+#define REQ(p)                                   \
+    do {                                         \
+        int _rc = require((p), __func__);        \
+        if (_rc != AERO_OK) return _rc;          \
+    } while (0)
+}  // namespace
+
+extern "C" {
+
+const char* aero_last_error(void) { return g_last_error.c_str(); }
+const char* aero_version(void) { return "aero_b200 0.1 (sm_100a, fp64)"; }
+int64_t aero_kernel_launches(void) { return (int64_t)launches_total(); }
+
+int aero_create(const aero_cfg* cfg, aero_sketch** out) {
+    REQ(cfg);
+    REQ(out);
+    return guard([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw CudaError("no CUDA device: the AeroSketch B200 path has no CPU fallback");
+        *out = new aero_sketch{new Sketch(*cfg), true};
+    });
+}
+int aero_destroy(aero_sketch* h) {
+    if (!h) return AERO_OK;
+    return guard([&] {
+        if (h->owned) delete h->s;
+        delete h;
+    });
+}
+int aero_set_theta(aero_sketch* h, double theta) {
+    REQ(h);
+    return guard([&] { h->s->set_theta(theta); });
+}
+int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
+                      const double* theta_per_row, aero_event* log_out) {
+    REQ(h);
+    if (n > 0) {
+        REQ(rows);
+        REQ(t);
+    }
+    return guard([&] { h->s->update_block(rows, false, n, ld, t, theta_per_row, log_out); });
+}
+int aero_update_block_device(aero_sketch* h, const double* rows_device, int64_t n, int64_t ld,
+                             const int64_t* t, const double* theta_per_row, aero_event* log_out) {
+    REQ(h);
+    if (n > 0) {
+        REQ(rows_device);
+        REQ(t);
+    }
+    return guard([&] { h->s->update_block(rows_device, true, n, ld, t, theta_per_row, log_out); });
+}
+int aero_query(aero_sketch* h, int64_t lb, int64_t ub, double* out) {
+    REQ(h);
+    REQ(out);
+    return guard([&] { h->s->query(lb, ub, out); });
+}
+int aero_query_gram(aero_sketch* h, int64_t lb, int64_t ub, double* out) {
+    REQ(h);
+    REQ(out);
+    return guard([&] { h->s->query_gram(lb, ub, out); });
+}
+int aero_attp_query(aero_sketch* h, int64_t t, double* out) {  // attp.hpp:29-32
+    REQ(h);
+    REQ(out);
+    return guard([&] {
+        if (t < 1 || t > h->s->clock()) throw InvalidInput("AttpState: t out of range");
+        h->s->query(0, t, out);
+    });
+}
+int aero_residual(aero_sketch* h, double* out, int64_t max_rows) {
+    REQ(h);
+    return guard([&] {
+        if (h->s->rows() > 0 && max_rows > 0) {
+            if (!out) throw InvalidInput("aero_residual: null output");
+            h->s->residual(out, max_rows);
+        }
+    });
+}
+int aero_snap_count(aero_sketch* h, int64_t* count) {
+    REQ(h);
+    REQ(count);
+    *count = h->s->snap_count();
+    return AERO_OK;
+}
+int aero_snap_info(aero_sketch* h, int64_t idx, int32_t* xi, int64_t* s, int64_t* t, double* theta) {
+    REQ(h);
+    return guard([&] {
+        const SnapRec& r = h->s->snap(idx);
+        if (xi) *xi = r.xi;
+        if (s) *s = r.s;
+        if (t) *t = r.t;
+        if (theta) *theta = r.theta;
+    });
+}
+int aero_snap_get(aero_sketch* h, int64_t idx, double* z, double* m) {
+    REQ(h);
+    return guard([&] { h->s->snap_get(idx, z, m); });
+}
+int aero_snap_pop_front(aero_sketch* h) {
+    REQ(h);
+    return guard([&] { h->s->snap_pop_front(); });
+}
+int aero_last_stats(aero_sketch* h, aero_event* out) {
+    REQ(h);
+    REQ(out);
+    *out = h->s->last_event();
+    return AERO_OK;
+}
+int aero_get_info(aero_sketch* h, aero_info* out) {
+    REQ(h);
+    REQ(out);
+    h->s->info(out);
+    return AERO_OK;
+}
+int aero_synchronize(aero_sketch* h) {
+    REQ(h);
+    return guard([&] { h->s->synchronize(); });
+}
+
+void* aero_stream(aero_sketch* h) { return h ? (void*)h->s->stream() : nullptr; }
+int aero_get_profile(aero_sketch* h, aero_profile* out) {
+    REQ(h);
+    REQ(out);
+    *out = h->s->prof;
+    return AERO_OK;
+}
+int aero_reset_profile(aero_sketch* h) {
+    REQ(h);
+    h->s->prof = aero_profile{};
+    return AERO_OK;
+}
+
+int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out) {
+    REQ(out);
+    return guard([&] {
+        uint64_t s = stream;
+        if (fork > 0) s = fork_stream(stream, (uint64_t)fork);
+        double* d = nullptr;
+        AERO_CUDA(cudaMalloc(&d, sizeof(double) * std::max<int64_t>(count, 1)));
+        gen_gaussian_matrix(0, rng_state0(seed, s), count, d);
+        AERO_CUDA(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
+        cudaFree(d);
+    });
+}
+
+// ---- MlState ----------------------------------------------------------------
+struct aero_ml {
+    MlEngine* e;
+    std::vector<aero_sketch> levels;
+};
+int aero_ml_create(int32_t d, int64_t window, double r_max, double eps, uint64_t seed,
+                   uint64_t stream, int32_t device, aero_ml** out) {
+    REQ(out);
+    return guard([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw CudaError("no CUDA device: the AeroSketch B200 path has no CPU fallback");
+        auto* h = new aero_ml;
+        h->e = new MlEngine(d, window, r_max, eps, seed, stream, device);
+        for (int j = 0; j < h->e->levels(); ++j) h->levels.push_back(aero_sketch{&h->e->level(j), false});
+        *out = h;
+    });
+}
+int aero_ml_destroy(aero_ml* h) {
+    if (!h) return AERO_OK;
+    return guard([&] {
+        delete h->e;
+        delete h;
+    });
+}
+int aero_ml_update_block(aero_ml* h, const double* rows, int64_t n, int64_t ld, const int64_t* t) {
+    REQ(h);
+    return guard([&] { h->e->update_block(rows, false, n, ld, t); });
+}
+int aero_ml_update_block_device(aero_ml* h, const double* rows, int64_t n, int64_t ld,
+                                const int64_t* t) {
+    REQ(h);
+    return guard([&] { h->e->update_block(rows, true, n, ld, t); });
+}
+int aero_ml_query(aero_ml* h, double* out, aero_ml_query_result* res) {
+    REQ(h);
+    REQ(out);
+    return guard([&] { h->e->query(out, res); });
+}
+int aero_ml_get_info(aero_ml* h, aero_ml_info* out) {
+    REQ(h);
+    REQ(out);
+    h->e->info(out);
+    return AERO_OK;
+}
+double aero_ml_theta(aero_ml* h, int32_t level) {
+    if (!h || level < 0 || level >= h->e->levels()) return -1.0;
+    return h->e->level(level).theta();
+}
+aero_sketch* aero_ml_level(aero_ml* h, int32_t level) {
+    if (!h || level < 0 || level >= (int)h->levels.size()) return nullptr;
+    return &h->levels[level];
+}
+int aero_ml_heavy_count(aero_ml* h, int32_t level, int64_t* count) {
+    REQ(h);
+    REQ(count);
+    return guard([&] { *count = h->e->heavy_count(level); });
+}
+int aero_ml_heavy_get(aero_ml* h, int32_t level, int64_t idx, double* row, int64_t* s, int64_t* t) {
+    REQ(h);
+    return guard([&] { h->e->heavy_get(level, idx, row, s, t); });
+}
+
+// ---- distributed ---------------------------------------------------------------
+int aero_dist_theta_schedule(int32_t m, int64_t T, double eps, int64_t latency,
+                             const double* sq_norms, double* theta_out, int64_t* mass_bytes,
+                             int64_t* broadcasts) {
+    REQ(sq_norms);
+    REQ(theta_out);
+    return guard([&] {
+        dist_theta_schedule(m, T, eps, latency, sq_norms, theta_out, mass_bytes, broadcasts);
+    });
+}
+struct aero_coord {
+    Coordinator* c;
+};
+int aero_coord_create(int32_t d, int32_t m, int32_t device, void* nccl_comm, aero_coord** out) {
+    REQ(out);
+    return guard([&] { *out = new aero_coord{new Coordinator(d, m, device, nccl_comm)}; });
+}
+int aero_coord_destroy(aero_coord* h) {
+    if (!h) return AERO_OK;
+    return guard([&] {
+        delete h->c;
+        delete h;
+    });
+}
+int aero_coord_absorb_snapshots(aero_coord* h, aero_sketch* site, int64_t* bytes) {
+    REQ(h);
+    REQ(site);
+    return guard([&] {
+        const int64_t b = h->c->absorb(*site->s);
+        if (bytes) *bytes = b;
+    });
+}
+int aero_coord_probe(aero_coord* h, aero_sketch* const* sites, int32_t nsites, int32_t root,
+                     int32_t ell, double* out, double* gram) {
+    REQ(h);
+    return guard([&] {
+        std::vector<Sketch*> ss;
+        for (int i = 0; i < nsites; ++i)
+            if (sites && sites[i]) ss.push_back(sites[i]->s);
+        h->c->probe(ss, root, ell, out, gram);
+    });
+}
+int aero_nccl_get_unique_id(char* id128) {
+    REQ(id128);
+    return guard([&] { nccl_unique_id(id128); });
+}
+int aero_nccl_comm_init(const char* id128, int32_t nranks, int32_t rank, int32_t device,
+                        void** comm_out) {
+    REQ(id128);
+    REQ(comm_out);
+    return guard([&] { *comm_out = nccl_comm_init(id128, nranks, rank, device); });
+}
+int aero_nccl_comm_destroy(void* comm) {
+    return guard([&] { nccl_comm_destroy(comm); });
+}
+
+// ---- CodState --------------------------------------------------------------
+struct aero_cod {
+    CodEngine* e;
+};
+int aero_cod_create(int32_t dx, int32_t dy, double eps, double theta, int64_t window,
+                    uint64_t seed, uint64_t stream, int32_t device, aero_cod** out) {
+    REQ(out);
+    return guard([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw CudaError("no CUDA device: the AeroSketch B200 path has no CPU fallback");
+        *out = new aero_cod{new CodEngine(dx, dy, eps, theta, window, seed, stream, device)};
+    });
+}
+int aero_cod_destroy(aero_cod* h) {
+    if (!h) return AERO_OK;
+    return guard([&] {
+        delete h->e;
+        delete h;
+    });
+}
+int aero_cod_update_block(aero_cod* h, const double* xs, const double* ys, int64_t n,
+                          const int64_t* t, aero_event* log_out) {
+    REQ(h);
+    return guard([&] { h->e->update_block(xs, ys, n, t, log_out); });
+}
+int aero_cod_query(aero_cod* h, double* astar, double* bstar) {
+    REQ(h);
+    return guard([&] { h->e->query(astar, bstar); });
+}
+int aero_cod_query_product(aero_cod* h, double* p) {
+    REQ(h);
+    return guard([&] { h->e->query_product(p); });
+}
+int aero_cod_info(aero_cod* h, int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock) {
+    REQ(h);
+    h->e->info(ell, cols, snaps, clock);
+    return AERO_OK;
+}
+
+// ---- generator -----------------------------------------------------------------
+int aero_gen_rows_device(const aero_gen_params* p, int64_t t0, int64_t n, double* out_device,
+                         int32_t device) {
+    REQ(p);
+    REQ(out_device);
+    return guard([&] { gen_rows_device(*p, t0, n, out_device, device); });
+}
+
+}  // extern "C"

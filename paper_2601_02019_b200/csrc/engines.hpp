@@ -1,0 +1,95 @@
+// Wrappers above the single-level Sketch: MlState (sliding window), the
+// distributed coordinator merge, the AMM CodState, and the stream generator.
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <vector>
+
+#include "../../include/aero_b200.h"
+#include "sketch.hpp"
+
+namespace aero_b200 {
+
+// ---- MlState (sliding_window.hpp:39-81, sliding_window.cpp:15-156) --------
+struct HeavyRow {
+    std::vector<double> row;
+    int64_t s, t;
+};
+class MlEngine {
+  public:
+    MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, uint64_t stream, int device);
+    void update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t);
+    void query(double* out_host, aero_ml_query_result* res);
+    void info(aero_ml_info* out) const;
+    int levels() const { return (int)levels_.size(); }
+    Sketch& level(int j) { return *levels_[j]; }
+    int64_t heavy_count(int j) const;
+    void heavy_get(int j, int64_t idx, double* row, int64_t* s, int64_t* t) const;
+
+  private:
+    struct LevelQueue {  // replay view of the combined per-level queue
+        int64_t avail = 0;  // snapshots at the front of the sketch deque created so far
+    };
+    int64_t combined_len(int j) const;
+    int64_t front_t(int j) const;
+    int64_t front_s(int j) const;
+    int64_t tail_t(int j) const;
+    void pop_front(int j);
+    int d_, ell_, dev_;
+    int64_t n_, cap_, clock_ = 0, norm_warnings_ = 0;
+    double r_max_, eps_, window_mass_ = 0.0;
+    std::vector<std::unique_ptr<Sketch>> levels_;
+    std::vector<std::deque<HeavyRow>> heavy_;
+    std::vector<LevelQueue> lq_;
+    std::deque<double> ring_;
+    DeviceBuf stage_, gather_, nrm_, out_, qa_, qb_;
+    cudaStream_t st_ = nullptr;
+};
+
+// ---- distributed (distributed.cpp:31-173) ---------------------------------
+void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const double* sq_norms,
+                         double* theta_out, int64_t* mass_bytes, int64_t* broadcasts);
+class Coordinator {
+  public:
+    Coordinator(int d, int m, int device, void* nccl_comm);
+    ~Coordinator();
+    int64_t absorb(Sketch& site);
+    void probe(const std::vector<Sketch*>& sites, int root, int ell, double* out_host, double* gram_host);
+
+  private:
+    int d_, m_, dev_;
+    void* comm_;
+    DeviceBuf B_, P_, W_, out_;
+    cudaStream_t st_ = nullptr;
+};
+void nccl_unique_id(char* id128);
+void* nccl_comm_init(const char* id128, int nranks, int rank, int device);
+void nccl_comm_destroy(void* comm);
+
+// ---- CodState (amm.hpp:35-69, amm.cpp:27-122) --------------------------------
+class CodEngine {
+  public:
+    CodEngine(int dx, int dy, double eps, double theta, int64_t n, uint64_t seed, uint64_t stream,
+              int device);
+    ~CodEngine();
+    void update_block(const double* xs, const double* ys, int64_t n, const int64_t* t,
+                      aero_event* log);
+    void query(double* astar, double* bstar);
+    void query_product(double* p);
+    void info(int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock) const;
+
+  private:
+    struct Impl;
+    Impl* im_;
+};
+
+// ---- generator ---------------------------------------------------------------
+void gen_rows_device(const aero_gen_params& p, int64_t t0, int64_t n, double* out, int device);
+
+// shrink_to_sketch on device: B (d x d, device, destroyed) -> out (ell x d
+// row-major, device)
+void shrink_device(cudaStream_t st, int d, int ell, double* B, double* w, double* out);
+
+}  // namespace aero_b200

@@ -1,0 +1,756 @@
+// B200 (sm_100a) device kernels for the AeroSketch update path.
+// fp64 throughout: the reference computes in fp64 (Eigen MatrixXd) and the
+// parity contract compares decision traces, which fp64 keeps bit-stable.
+#include <algorithm>
+#include <atomic>
+
+#include "aero_common.cuh"
+#include "kernels.cuh"
+
+namespace aero_b200 {
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launches_total() { return g_launches.load(); }
+
+// ============================================================================
+// fp64 GEMM (column-major): D = alpha op(A) op(B) + beta D, optional row mask
+// per output column (rows >= colmask[j] written as 0). Register-blocked DFMA
+// with double-buffered shared-memory tiles; micro-tile rows/cols are strided
+// so that a warp's shared-memory reads are conflict-free.
+// ============================================================================
+template <int BM, int BN, int BK, int TM, int TN, bool TA, bool TB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    k_dgemm(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
+            const double* __restrict__ B, int ldb, double beta, double* __restrict__ D, int ldd,
+            const int* __restrict__ colmask) {
+    constexpr int RT = BM / TM, CT = BN / TN, NT = RT * CT;
+    constexpr int LA = (BM * BK) / NT, LB = (BK * BN) / NT;
+    static_assert((BM * BK) % NT == 0 && (BK * BN) % NT == 0, "tile/thread mismatch");
+    __shared__ double As[2][BK][BM];
+    __shared__ double Bs[2][BK][BN];
+    const int tid = threadIdx.x;
+    const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
+    const int tr = tid % RT, tc = tid / RT;
+    double acc[TM][TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
+    double ra[LA], rb[LB];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int s = 0; s < LA; ++s) {
+            const int e = tid + s * NT;
+            int i, l;
+            if (!TA) { i = e % BM; l = e / BM; } else { l = e % BK; i = e / BK; }
+            const int gi = bm + i, gl = k0 + l;
+            double v = 0.0;
+            if (gi < m && gl < k) v = TA ? A[gl + (int64_t)gi * lda] : A[gi + (int64_t)gl * lda];
+            ra[s] = v;
+        }
+#pragma unroll
+        for (int s = 0; s < LB; ++s) {
+            const int e = tid + s * NT;
+            int j, l;
+            if (!TB) { l = e % BK; j = e / BK; } else { j = e % BN; l = e / BN; }
+            const int gj = bn + j, gl = k0 + l;
+            double v = 0.0;
+            if (gj < n && gl < k) v = TB ? B[gj + (int64_t)gl * ldb] : B[gl + (int64_t)gj * ldb];
+            rb[s] = v;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int s = 0; s < LA; ++s) {
+            const int e = tid + s * NT;
+            int i, l;
+            if (!TA) { i = e % BM; l = e / BM; } else { l = e % BK; i = e / BK; }
+            As[buf][l][i] = ra[s];
+        }
+#pragma unroll
+        for (int s = 0; s < LB; ++s) {
+            const int e = tid + s * NT;
+            int j, l;
+            if (!TB) { l = e % BK; j = e / BK; } else { j = e % BN; l = e / BN; }
+            Bs[buf][l][j] = rb[s];
+        }
+    };
+    const int nk = (k + BK - 1) / BK;
+    if (nk > 0) {
+        load(0);
+        store(0);
+    }
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+        const int cur = kt & 1;
+        if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            double av[TM], bv[TN];
+#pragma unroll
+            for (int a = 0; a < TM; ++a) av[a] = As[cur][kk][tr + a * RT];
+#pragma unroll
+            for (int b = 0; b < TN; ++b) bv[b] = Bs[cur][kk][tc + b * CT];
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+        if (kt + 1 < nk) store(cur ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+        const int gj = bn + tc + b * CT;
+        if (gj >= n) continue;
+        const int lim = colmask ? colmask[gj] : m;
+#pragma unroll
+        for (int a = 0; a < TM; ++a) {
+            const int gi = bm + tr + a * RT;
+            if (gi >= m) continue;
+            double* p = D + gi + (int64_t)gj * ldd;
+            double v = alpha * acc[a][b];
+            if (beta != 0.0) v = fma(beta, *p, v);
+            if (gi >= lim) v = 0.0;
+            *p = v;
+        }
+    }
+}
+
+template <int BM, int BN, int TM, int TN>
+static void launch_gemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha,
+                        const double* A, int lda, const double* B, int ldb, double beta, double* D,
+                        int ldd, const int* colmask) {
+    constexpr int NT = (BM / TM) * (BN / TN);
+    dim3 grid((n + BN - 1) / BN, (m + BM - 1) / BM);
+    if (!ta && !tb)
+        k_dgemm<BM, BN, 16, TM, TN, false, false><<<grid, NT, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+    else if (ta && !tb)
+        k_dgemm<BM, BN, 16, TM, TN, true, false><<<grid, NT, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+    else if (!ta && tb)
+        k_dgemm<BM, BN, 16, TM, TN, false, true><<<grid, NT, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+    else
+        k_dgemm<BM, BN, 16, TM, TN, true, true><<<grid, NT, 0, st>>>(m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+    AERO_LAUNCHED();
+}
+
+void dgemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha, const double* A,
+           int lda, const double* B, int ldb, double beta, double* D, int ldd,
+           const int* colmask) {
+    if (m <= 0 || n <= 0) return;
+    const long long big = (long long)((m + 63) / 64) * ((n + 63) / 64);
+    if (big >= 120)
+        launch_gemm<64, 64, 4, 4>(st, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+    else
+        launch_gemm<32, 32, 2, 2>(st, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, D, ldd, colmask);
+}
+
+// ============================================================================
+// ingestion (K1): per-row squared norm + finiteness, one warp per row,
+// coalesced 8-byte loads (reference sketch.cpp:83-84, attp.hpp:22)
+// ============================================================================
+__global__ void k_ingest(const double* __restrict__ rows, int64_t n, int64_t ld, int d,
+                         double* __restrict__ nrm2, int* __restrict__ bad) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const double* a = rows + row * ld;
+    double s = 0.0;
+    int nf = 0;
+    for (int j = lane; j < d; j += 32) {
+        const double v = a[j];
+        nf |= !isfinite(v);
+        s = fma(v, v, s);
+    }
+    s = warp_sum(s);
+    nf = __any_sync(0xffffffffu, nf);
+    if (lane == 0) {
+        nrm2[row] = s;
+        bad[row] = nf;
+    }
+}
+void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int d, double* nrm2,
+                 int* bad) {
+    if (n <= 0) return;
+    const int wpb = 8;
+    k_ingest<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(rows, n, ld, d, nrm2, bad);
+    AERO_LAUNCHED();
+}
+
+// ============================================================================
+// CTA-wide cyclic Jacobi for small symmetric matrices in shared memory
+// (round-robin parallel ordering; A, V column-major n x n, ld = n).
+// On return diag(A) holds the eigenvalues (unsorted) and V the eigenvectors.
+// ============================================================================
+struct JacobiScratch {
+    double* cs;   // 2 * (n/2+1)
+    int* flag;    // 1
+};
+__device__ void cta_jacobi(double* A, double* V, int n, JacobiScratch sc) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < n * n; e += nt) V[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
+    __syncthreads();
+    if (n <= 1) return;
+    const int np = n + (n & 1);  // players (dummy = n when odd)
+    const int half = np / 2;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (tid == 0) *sc.flag = 0;
+        __syncthreads();
+        for (int step = 0; step < np - 1; ++step) {
+            // (a) rotation parameters for the disjoint pairs of this step
+            for (int i = tid; i < half; i += nt) {
+                const int pi = (i == 0) ? 0 : ((i - 1 + step) % (np - 1)) + 1;
+                const int qi = ((np - 1 - i - 1 + step) % (np - 1)) + 1;
+                int p = min(pi, qi), q = max(pi, qi);
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double apq = A[p + q * n];
+                    const double app = A[p + p * n], aqq = A[q + q * n];
+                    if (fabs(apq) > 1e-300 &&
+                        fabs(apq) > 1.1102230246251565e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        *sc.flag = 1;
+                    }
+                }
+                sc.cs[2 * i] = c;
+                sc.cs[2 * i + 1] = s;
+            }
+            __syncthreads();
+            // (b) A <- R^T A R on 2x2 blocks of pair pairs; V <- V R
+            const int nblk = half * half;
+            for (int bidx = tid; bidx < nblk + half * n; bidx += nt) {
+                if (bidx < nblk) {
+                    const int I = bidx % half, J = bidx / half;
+                    const int pI0 = (I == 0) ? 0 : ((I - 1 + step) % (np - 1)) + 1;
+                    const int qI0 = ((np - 1 - I - 1 + step) % (np - 1)) + 1;
+                    const int pJ0 = (J == 0) ? 0 : ((J - 1 + step) % (np - 1)) + 1;
+                    const int qJ0 = ((np - 1 - J - 1 + step) % (np - 1)) + 1;
+                    const int p = min(pI0, qI0), q = max(pI0, qI0);
+                    const int pp = min(pJ0, qJ0), qq = max(pJ0, qJ0);
+                    const double cI = sc.cs[2 * I], sI = sc.cs[2 * I + 1];
+                    const double cJ = sc.cs[2 * J], sJ = sc.cs[2 * J + 1];
+                    const bool qin = q < n, qqin = qq < n;
+                    const double b00 = A[p + pp * n];
+                    const double b01 = qqin ? A[p + qq * n] : 0.0;
+                    const double b10 = qin ? A[q + pp * n] : 0.0;
+                    const double b11 = (qin && qqin) ? A[q + qq * n] : 0.0;
+                    // left: rows (p,q) by R^T = [[c,-s],[s,c]]
+                    const double l00 = cI * b00 - sI * b10, l01 = cI * b01 - sI * b11;
+                    const double l10 = sI * b00 + cI * b10, l11 = sI * b01 + cI * b11;
+                    // right: cols (pp,qq) by R = [[c,s],[-s,c]]
+                    A[p + pp * n] = cJ * l00 - sJ * l01;
+                    if (qqin) A[p + qq * n] = sJ * l00 + cJ * l01;
+                    if (qin) A[q + pp * n] = cJ * l10 - sJ * l11;
+                    if (qin && qqin) A[q + qq * n] = sJ * l10 + cJ * l11;
+                } else {
+                    const int e = bidx - nblk;
+                    const int I = e % half, row = e / half;
+                    const int pI0 = (I == 0) ? 0 : ((I - 1 + step) % (np - 1)) + 1;
+                    const int qI0 = ((np - 1 - I - 1 + step) % (np - 1)) + 1;
+                    const int p = min(pI0, qI0), q = max(pI0, qI0);
+                    if (q >= n) continue;
+                    const double c = sc.cs[2 * I], s = sc.cs[2 * I + 1];
+                    const double vp = V[row + p * n], vq = V[row + q * n];
+                    V[row + p * n] = c * vp - s * vq;
+                    V[row + q * n] = s * vp + c * vq;
+                }
+            }
+            __syncthreads();
+        }
+        if (*sc.flag == 0) break;
+        __syncthreads();
+    }
+    __syncthreads();
+}
+
+// sort eigenpairs descending (stable rank sort) from (A diag, V) into (w, Vout)
+// and fix eigenvector signs (largest-magnitude entry positive, first on ties)
+__device__ void cta_sort_signfix(const double* A, const double* V, int n, double* w, double* Vout,
+                                 int ldvo) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < n; i += nt) {
+        const double li = A[i + i * n];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double lj = A[j + j * n];
+            rank += (lj > li) || (lj == li && j < i);
+        }
+        w[rank] = li;
+        // sign fix of column i
+        int at = 0;
+        double best = -1.0;
+        for (int r = 0; r < n; ++r) {
+            const double v = fabs(V[r + i * n]);
+            if (v > best) { best = v; at = r; }
+        }
+        const double sg = (V[at + i * n] < 0.0) ? -1.0 : 1.0;
+        for (int r = 0; r < n; ++r) Vout[r + (int64_t)rank * ldvo] = sg * V[r + i * n];
+    }
+    __syncthreads();
+}
+
+__global__ void k_jacobi_batched(int n, double* A, int lda, int64_t stride, double* w) {
+    extern __shared__ double sm[];
+    double* sA = sm;
+    double* sV = sA + n * n;
+    double* cs = sV + n * n;
+    int* flag = reinterpret_cast<int*>(cs + 2 * (n / 2 + 2));
+    double* Ab = A + blockIdx.x * stride;
+    double* wb = w + blockIdx.x * (int64_t)n;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e % n, j = e / n;
+        sA[e] = 0.5 * (Ab[i + (int64_t)j * lda] + Ab[j + (int64_t)i * lda]);
+    }
+    __syncthreads();
+    cta_jacobi(sA, sV, n, JacobiScratch{cs, flag});
+    cta_sort_signfix(sA, sV, n, wb, Ab, lda);
+}
+
+void eigh_small(cudaStream_t st, int n, double* A, int lda, double* w, int batch, int64_t stride) {
+    const size_t smem = sizeof(double) * (2 * n * n + 2 * (n / 2 + 2)) + 16;
+    if (smem > 48 * 1024)
+        AERO_CUDA(cudaFuncSetAttribute(k_jacobi_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    k_jacobi_batched<<<batch, 256, smem, st>>>(n, A, lda, stride, w);
+    AERO_LAUNCHED();
+}
+
+// ============================================================================
+// batched power / subspace iteration engine (gate K2 + simul_iter K4)
+// ============================================================================
+__global__ void k_iter_init(const IterJob* __restrict__ jobs, const double* __restrict__ G, int ldg,
+                            double* __restrict__ X, int ldx, int R, int* __restrict__ status) {
+    __shared__ double red[32];
+    const IterJob jb = jobs[blockIdx.x];
+    double tr = 0.0;
+    for (int i = threadIdx.x; i < jb.r; i += blockDim.x) tr += G[i + (int64_t)i * ldg];
+    tr = block_sum(tr, red);
+    const bool zero = (tr == 0.0);
+    if (threadIdx.x == 0) status[blockIdx.x] = zero ? JOB_ZERO : JOB_ACTIVE;
+    double ss = 0.0;
+    for (int j = 0; j < jb.k; ++j) {
+        double* x = X + (int64_t)(jb.col + j) * ldx;
+        for (int i = threadIdx.x; i < R; i += blockDim.x) {
+            double v = 0.0;
+            if (i < jb.r && !zero) v = rng_gaussian_at(jb.rng0, (uint64_t)i * jb.k + j);
+            x[i] = v;
+            ss = fma(v, v, ss);
+        }
+    }
+    if (jb.type == 0 && !zero) {  // gate: x.normalize() (linalg.cpp:108)
+        ss = block_sum(ss, red);
+        const double nrm = sqrt(ss);
+        double* x = X + (int64_t)jb.col * ldx;
+        if (nrm > 0.0)
+            for (int i = threadIdx.x; i < jb.r; i += blockDim.x) x[i] = x[i] / nrm;
+    }
+}
+void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg,
+               double* X, int ldx, int R, int* status) {
+    if (njobs <= 0) return;
+    k_iter_init<<<njobs, 256, 0, st>>>(jobs, G, ldg, X, ldx, R, status);
+    AERO_LAUNCHED();
+}
+
+// k x k Gram of two column blocks P (r x k) and Q (r x k), ld, into S (smem, col-major)
+__device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k, double* S,
+                         double* red) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int E = k * k;
+    if (E <= 16) {
+        double part[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) part[e] = 0.0;
+        for (int i = tid; i < r; i += nt) {
+            double p[4], q[4];
+            for (int a = 0; a < k; ++a) {
+                p[a] = P[i + (int64_t)a * ld];
+                q[a] = Q[i + (int64_t)a * ld];
+            }
+            for (int a = 0; a < k; ++a)
+                for (int b = 0; b < k; ++b) part[a + b * k] = fma(p[a], q[b], part[a + b * k]);
+        }
+        const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
+        for (int e = 0; e < E; ++e) {
+            const double v = warp_sum(part[e]);
+            if (lane == 0) red[wid * 16 + e] = v;
+        }
+        __syncthreads();
+        for (int e = tid; e < E; e += nt) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w * 16 + e];
+            S[e] = t;
+        }
+        __syncthreads();
+    } else {
+        // one thread per entry, rows streamed (k up to 64; rare path)
+        for (int e = tid; e < E; e += nt) {
+            const int a = e % k, b = e / k;
+            double t = 0.0;
+            for (int i = 0; i < r; ++i) t = fma(P[i + (int64_t)a * ld], Q[i + (int64_t)b * ld], t);
+            S[e] = t;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, double* X,
+                                 const double* __restrict__ Y, int ldx, double* H,
+                                 int* __restrict__ status, double* __restrict__ out_sig,
+                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
+                                 int max_k) {
+    extern __shared__ double sm[];
+    const IterJob jb = jobs[blockIdx.x];
+    if (phase >= jb.nphase) return;
+    const int st = status[blockIdx.x];
+    const bool last = (phase == jb.nphase - 1);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int r = jb.r, k = jb.k;
+    double* x = X + (int64_t)jb.col * ldx;
+    const double* y = Y + (int64_t)jb.col * ldx;
+    double* red = sm;                       // 32*16
+    double* S = red + 32 * 16;              // k*k
+    double* W = S + max_k * max_k;          // k*k
+    double* T = W + max_k * max_k;          // k*k
+    double* lam = T + max_k * max_k;        // k
+    double* cs = lam + max_k;               // 2*(k/2+2)
+    int* flag = reinterpret_cast<int*>(cs + 2 * (max_k / 2 + 2));
+    if (st != JOB_ACTIVE) {
+        if (last && tid == 0) {
+            if (jb.type == 0) out_sig[jb.col] = 0.0;
+            else
+                for (int a = 0; a < k; ++a) out_sig[jb.col + a] = 0.0;
+        }
+        return;
+    }
+    if (jb.type == 0) {
+        if (!last) {
+            double s = 0.0;
+            for (int i = tid; i < r; i += nt) s = fma(y[i], y[i], s);
+            s = block_sum(s, red);
+            const double nrm = sqrt(s);
+            if (nrm < 1e-300) {  // linalg.cpp:112-116
+                if (tid == 0) status[blockIdx.x] = JOB_DEAD;
+                return;
+            }
+            for (int i = tid; i < r; i += nt) x[i] = y[i] / nrm;
+        } else {
+            double s = 0.0;  // sigma1^2 = ||A x||^2 = x^T G x (linalg.cpp:119)
+            for (int i = tid; i < r; i += nt) s = fma(x[i], y[i], s);
+            s = block_sum(s, red);
+            if (tid == 0) out_sig[jb.col] = s;
+        }
+        return;
+    }
+    // simul: S = X^T Y (Gram of g = C'^T X), T = S^{-1/2}
+    cta_gram(x, y, ldx, r, k, S, red);
+    for (int e = tid; e < k * k; e += nt) {
+        const int a = e % k, b = e / k;
+        W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
+    }
+    __syncthreads();
+    cta_jacobi(W, T, k, JacobiScratch{cs, flag});  // W -> diag, T -> eigvecs
+    // lam_i and T columns scaled by lam^{-1/2} with clamp
+    if (tid == 0) {
+        double lmax = 0.0;
+        for (int i = 0; i < k; ++i) lmax = fmax(lmax, W[i + i * k]);
+        int nclamp = 0;
+        for (int i = 0; i < k; ++i) {
+            const double l = W[i + i * k];
+            const bool ok = l > 0.0 && l > 1e-14 * lmax;
+            lam[i] = ok ? 1.0 / sqrt(l) : 0.0;
+            nclamp += !ok;
+        }
+        if (last && out_clamped) out_clamped[blockIdx.x] = nclamp;
+    }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
+    __syncthreads();
+    // rows independent: [last: H = X T], X <- Y T
+    for (int i = tid; i < r; i += nt) {
+        double xr[64], yr[64];
+        for (int a = 0; a < k; ++a) {
+            xr[a] = x[i + (int64_t)a * ldx];
+            yr[a] = y[i + (int64_t)a * ldx];
+        }
+        for (int b = 0; b < k; ++b) {
+            double hx = 0.0, hy = 0.0;
+            for (int a = 0; a < k; ++a) {
+                hx = fma(xr[a], T[a + b * k], hx);
+                hy = fma(yr[a], T[a + b * k], hy);
+            }
+            if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;
+            x[i + (int64_t)b * ldx] = hy;
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    // Ritz values: eig(w^T w), w = C' g = G H = X (linalg.cpp:145-150)
+    cta_gram(x, x, ldx, r, k, S, red);
+    for (int e = tid; e < k * k; e += nt) {
+        const int a = e % k, b = e / k;
+        W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
+    }
+    __syncthreads();
+    cta_jacobi(W, T, k, JacobiScratch{cs, flag});
+    double* vr = out_vr + (int64_t)jb.col * kv;
+    cta_sort_signfix(W, T, k, lam, vr, k);
+    for (int a = tid; a < k; a += nt) out_sig[jb.col + a] = sqrt(fmax(lam[a], 0.0));
+}
+
+void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
+                    const double* Y, int ldx, double* H, int* status, double* out_sig,
+                    double* out_vr, int kv, int* out_clamped, int max_k) {
+    if (njobs <= 0) return;
+    const size_t smem =
+        sizeof(double) * (32 * 16 + 3 * max_k * max_k + max_k + 2 * (max_k / 2 + 2)) + 16;
+    if (smem > 48 * 1024)
+        AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    k_iter_normalize<<<njobs, 256, smem, st>>>(jobs, phase, X, Y, ldx, H, status, out_sig, out_vr,
+                                               kv, out_clamped, max_k);
+    AERO_LAUNCHED();
+}
+
+// ============================================================================
+// small helpers
+// ============================================================================
+__global__ void k_scale_columns(int n, int ncol, double* V, int ld, const double* scale) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)n * ncol) return;
+    const int i = (int)(e % n), j = (int)(e / n);
+    V[i + (int64_t)j * ld] *= scale[j];
+}
+void scale_columns(cudaStream_t st, int n, int ncol, double* V, int ld, const double* scale) {
+    const int64_t tot = (int64_t)n * ncol;
+    if (tot <= 0) return;
+    k_scale_columns<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, ncol, V, ld, scale);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_fd_weights(const double* lam, int n, int ell, int keep, double* w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= keep) return;
+    const double si = sqrt(fmax(lam[i], 0.0));
+    double cut = 0.0;
+    if (ell <= n) {
+        const double se = sqrt(fmax(lam[ell - 1], 0.0));
+        cut = se * se;
+    }
+    const double s2 = si * si - cut;
+    w[i] = (s2 > 0.0 && si > 0.0) ? sqrt(s2) / si : 0.0;
+}
+void fd_weights(cudaStream_t st, const double* lam, int n, int ell, int keep, double* w) {
+    k_fd_weights<<<(keep + 127) / 128, 128, 0, st>>>(lam, n, ell, keep, w);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_fix_signs(int d, double* Z, int ld, double* flips) {
+    __shared__ double bv[32];
+    __shared__ int bi[32];
+    double* z = Z + (int64_t)blockIdx.x * ld;
+    double best = -1.0;
+    int at = 0x7fffffff;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const double v = fabs(z[i]);
+        if (v > best) { best = v; at = i; }
+    }
+    // warp argmax with first-index tie break
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, at, o);
+        if (ov > best || (ov == best && oi < at)) { best = ov; at = oi; }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) { bv[wid] = best; bi[wid] = at; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w)
+            if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
+    }
+    __syncthreads();
+    const double sg = (bi[0] < d && z[bi[0]] < 0.0) ? -1.0 : 1.0;
+    __syncthreads();
+    if (sg < 0.0)
+        for (int i = threadIdx.x; i < d; i += blockDim.x) z[i] = -z[i];
+    if (threadIdx.x == 0 && flips) flips[blockIdx.x] = sg;
+}
+void fix_column_signs(cudaStream_t st, int d, int k, double* Z, int ld, double* flips) {
+    if (k <= 0) return;
+    k_fix_signs<<<k, 256, 0, st>>>(d, Z, ld, flips);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_symmetrize(int n, double* A, int lda) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)n * n) return;
+    const int i = (int)(e % n), j = (int)(e / n);
+    if (i >= j) return;
+    const double v = 0.5 * (A[i + (int64_t)j * lda] + A[j + (int64_t)i * lda]);
+    A[i + (int64_t)j * lda] = v;
+    A[j + (int64_t)i * lda] = v;
+}
+void symmetrize(cudaStream_t st, int n, double* A, int lda) {
+    const int64_t tot = (int64_t)n * n;
+    if (tot <= 0) return;
+    k_symmetrize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, A, lda);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_fill(double* p, int64_t count) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < count) p[e] = 0.0;
+}
+void fill_zero(cudaStream_t st, double* p, int64_t count) {
+    if (count <= 0) return;
+    k_fill<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(p, count);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_copy_matrix(int m, int n, const double* A, int lda, double* B, int ldb) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)m * n) return;
+    const int i = (int)(e % m), j = (int)(e / m);
+    B[i + (int64_t)j * ldb] = A[i + (int64_t)j * lda];
+}
+void copy_matrix(cudaStream_t st, int m, int n, const double* A, int lda, double* B, int ldb) {
+    const int64_t tot = (int64_t)m * n;
+    if (tot <= 0) return;
+    k_copy_matrix<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(m, n, A, lda, B, ldb);
+    AERO_LAUNCHED();
+}
+
+void rows_to_cols(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int d, double* Ct,
+                  int ldc) {
+    if (n <= 0) return;
+    AERO_CUDA(cudaMemcpy2DAsync(Ct, sizeof(double) * ldc, rows, sizeof(double) * ld,
+                                sizeof(double) * d, n, cudaMemcpyDefault, st));
+}
+
+__global__ void k_add_identity(int k, double* A, int lda, double alpha) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) A[i + (int64_t)i * lda] += alpha;
+}
+void add_identity(cudaStream_t st, int k, double* A, int lda, double alpha) {
+    if (k <= 0) return;
+    k_add_identity<<<(k + 127) / 128, 128, 0, st>>>(k, A, lda, alpha);
+    AERO_LAUNCHED();
+}
+
+__global__ void k_shrink_rows(const double* lam, const double* V, int ldv, int d, int ell,
+                              double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)ell * d) return;
+    const int i = (int)(e / d), j = (int)(e % d);
+    double v = 0.0;
+    if (i < d) {
+        const double cut = (ell <= d) ? fmax(lam[ell - 1], 0.0) : 0.0;
+        const double w = fmax(lam[i], 0.0) - cut;
+        if (w > 0.0) v = sqrt(w) * V[j + (int64_t)i * ldv];
+    }
+    out[e] = v;
+}
+void shrink_rows(cudaStream_t st, const double* lam, const double* V, int ldv, int d, int ell,
+                 double* out_rm) {
+    const int64_t tot = (int64_t)ell * d;
+    if (tot <= 0) return;
+    k_shrink_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lam, V, ldv, d, ell, out_rm);
+    AERO_LAUNCHED();
+}
+
+// restore contribution K terms: K_s = Mt_s^T Z_s (xi x xi), Y_s = Z_s K_s
+__global__ void k_restore_k(int d, const double* __restrict__ Z, const double* __restrict__ Mt,
+                            int ld, const int* __restrict__ offsets, const int* __restrict__ widths,
+                            double* __restrict__ Y) {
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    const int off = offsets[blockIdx.x], xi = widths[blockIdx.x];
+    double* K = sm;  // xi*xi
+    for (int a = 0; a < xi; ++a)
+        for (int b = 0; b < xi; ++b) {
+            double t = 0.0;
+            for (int i = threadIdx.x; i < d; i += blockDim.x)
+                t = fma(Mt[i + (int64_t)(off + a) * ld], Z[i + (int64_t)(off + b) * ld], t);
+            t = block_sum(t, red);
+            if (threadIdx.x == 0) K[a + b * xi] = t;
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+        for (int b = 0; b < xi; ++b) {
+            double t = 0.0;
+            for (int a = 0; a < xi; ++a) t = fma(Z[i + (int64_t)(off + a) * ld], K[a + b * xi], t);
+            Y[i + (int64_t)(off + b) * ld] = t;
+        }
+}
+void restore_k_terms(cudaStream_t st, int d, const double* Z, const double* Mt, int ld,
+                     const int* offsets, const int* widths, int nsnap, double* Y) {
+    // widths are bounded by the caller (xi <= kRestoreMaxXi per snapshot)
+    if (nsnap <= 0) return;
+    const size_t smem = sizeof(double) * 64 * 64;
+    k_restore_k<<<nsnap, 256, smem, st>>>(d, Z, Mt, ld, offsets, widths, Y);
+    AERO_LAUNCHED();
+}
+
+// ============================================================================
+// stream generator (DESIGN.md GENERATOR spec): one CTA per row
+// ============================================================================
+__global__ void k_gen_rows(int d, int k, int k2, const double* __restrict__ U1,
+                           const double* __restrict__ U2, double rho, double rho2, double scale2,
+                           double noise, double r_max, uint64_t seed, uint64_t stream, int64_t t0,
+                           double* __restrict__ out) {
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    double* coef = sm;          // k + k2
+    const int64_t t = t0 + blockIdx.x;
+    const uint64_t s0 = rng_state0(seed, (stream << 32) + (uint64_t)t);
+    for (int l = threadIdx.x; l < k + k2; l += blockDim.x) coef[l] = rng_gaussian_at(s0, l);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sig = 1.0;
+        for (int l = 0; l < k; ++l) { coef[l] *= sig; sig *= rho; }
+        sig = scale2;
+        for (int l = 0; l < k2; ++l) { coef[k + l] *= sig; sig *= rho2; }
+    }
+    __syncthreads();
+    double* a = out + (int64_t)blockIdx.x * d;
+    double ss = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double v = noise * rng_gaussian_at(s0, (uint64_t)(k + k2 + j));
+        for (int l = 0; l < k; ++l) v += coef[l] * U1[(int64_t)l * d + j];
+        for (int l = 0; l < k2; ++l) v += coef[k + l] * U2[(int64_t)l * d + j];
+        a[j] = v;
+        ss = fma(v, v, ss);
+    }
+    ss = block_sum(ss, red);
+    const uint64_t g = (uint64_t)(k + k2 + d);
+    const double u = rng_uniform_at(s0, 2 * ((g + 1) / 2) + 1);
+    const double scale = sqrt(pow(r_max, u) / ss);
+    for (int j = threadIdx.x; j < d; j += blockDim.x) a[j] *= scale;
+}
+void gen_rows(cudaStream_t st, int d, int k, int k2, const double* U1, const double* U2,
+              double rho, double rho2, double scale2, double noise, double r_max, uint64_t seed,
+              uint64_t stream, int64_t t0, int64_t n, double* out) {
+    for (int64_t off = 0; off < n; off += 1 << 20) {
+        const int64_t cnt = std::min<int64_t>(n - off, 1 << 20);
+        k_gen_rows<<<(unsigned)cnt, 256, sizeof(double) * (k + k2 + 1), st>>>(
+            d, k, k2, U1, U2, rho, rho2, scale2, noise, r_max, seed, stream, t0 + off,
+            out + off * d);
+        AERO_LAUNCHED();
+    }
+}
+
+__global__ void k_gen_gauss(uint64_t s0, int64_t count, double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < count) out[e] = rng_gaussian_at(s0, (uint64_t)e);
+}
+void gen_gaussian_matrix(cudaStream_t st, uint64_t state0, int64_t count, double* out) {
+    if (count <= 0) return;
+    k_gen_gauss<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(state0, count, out);
+    AERO_LAUNCHED();
+}
+
+}  // namespace aero_b200

@@ -1,0 +1,775 @@
+// AeroState engine on one B200 (see sketch.hpp). Control flow restates
+// /root/reference/proj/src/sketch.cpp:82-141 row by row; device work is
+// batched speculatively across rows.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "aero_common.cuh"
+#include "sketch.hpp"
+
+namespace aero_b200 {
+
+void DeviceBuf::alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    AERO_CUDA(cudaMalloc(&p, sizeof(double) * std::max<size_t>(count, 1)));
+    n = count;
+}
+void DeviceBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+}
+
+namespace {
+int power_iter_count(int d) {  // sketch.cpp:16-18
+    return static_cast<int>(std::ceil(std::log2(static_cast<double>(std::max(d, 2))))) + 1;
+}
+int simul_q(int d, double eps_si) {  // linalg.cpp:138-139
+    return static_cast<int>(
+        std::ceil(1.0 * std::log2(static_cast<double>(std::max(d, 2))) / eps_si));
+}
+template <typename T>
+T* pinned(size_t n) {
+    T* p = nullptr;
+    AERO_CUDA(cudaMallocHost(&p, sizeof(T) * std::max<size_t>(n, 1)));
+    return p;
+}
+template <typename T>
+T* dev_alloc(size_t n) {
+    T* p = nullptr;
+    AERO_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+    return p;
+}
+}  // namespace
+
+__global__ void k_sym_fill(int r0, int B, double* G, int ldg) {
+    // G[r0+j, i] = G[i, r0+j] for i < r0 (lower-left block of the new rows)
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)r0 * B) return;
+    const int i = (int)(e % r0), j = (int)(e / r0);
+    G[(r0 + j) + (int64_t)i * ldg] = G[i + (int64_t)(r0 + j) * ldg];
+}
+__global__ void k_inv_sqrt_clamp(const double* lam, int k, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double lmax = 0.0;
+    for (int i = 0; i < k; ++i) lmax = fmax(lmax, lam[i]);
+    for (int i = 0; i < k; ++i) {
+        const double l = lam[i];
+        out[i] = (l > 0.0 && l > 1e-14 * lmax) ? 1.0 / sqrt(l) : 0.0;
+    }
+}
+__global__ void k_sqrt_clamp(const double* lam, int k, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) out[i] = sqrt(fmax(lam[i], 0.0));
+}
+__global__ void k_identity_cols(int d, int xi, double* z, int ld) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)d * xi) return;
+    const int i = (int)(e % d), j = (int)(e / d);
+    z[i + (int64_t)j * ld] = (i == j) ? 1.0 : 0.0;
+}
+
+Sketch::Sketch(const aero_cfg& cfg) {
+    if (cfg.d < 1) throw InvalidInput("AeroState: d must be >= 1");
+    if (!(cfg.eps > 0.0 && cfg.eps <= 1.0)) throw InvalidInput("AeroState: eps out of (0,1]");
+    if (cfg.theta < 0.0) throw InvalidInput("AeroState: theta must be >= 0");
+    d_ = cfg.d;
+    eps_ = cfg.eps;
+    ell_ = cfg.ell > 0 ? cfg.ell : static_cast<int>(std::ceil(2.0 / cfg.eps));  // sketch.cpp:30
+    eps_si_ = cfg.eps_si > 0.0 ? cfg.eps_si : 0.4;                              // sketch.cpp:23
+    if (!(eps_si_ > 0.0 && eps_si_ < 1.0)) throw InvalidInput("AeroState: eps_si out of (0,1)");
+    theta_ = cfg.theta;
+    seed_ = cfg.seed;
+    stream_ = cfg.stream;
+    mode_ = cfg.theta_mode;
+    exact_ = (cfg.flags & AERO_FLAG_EXACT) != 0;
+    profiling = (cfg.flags & AERO_FLAG_PROFILE) != 0;
+    dev_ = cfg.device;
+    cap_ = 2 * ell_;
+    kp_ = power_iter_count(d_);
+    q_ = simul_q(d_, eps_si_);
+    max_batch_ = cfg.max_batch > 0 ? cfg.max_batch : 64;
+    AERO_CUDA(cudaSetDevice(dev_));
+    AERO_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    C_.alloc((size_t)d_ * cap_);
+    C2_.alloc((size_t)d_ * cap_);
+    G_.alloc((size_t)cap_ * cap_);
+    fill_zero(st_, G_.p, (int64_t)cap_ * cap_);
+    ldx_ = cap_;
+    ncols_ = std::max(3 * max_batch_, 64);
+    X_.alloc((size_t)ldx_ * ncols_);
+    Y_.alloc((size_t)ldx_ * ncols_);
+    H_.alloc((size_t)ldx_ * ncols_);
+    sig_.alloc(ncols_);
+    vr_.alloc((size_t)ncols_ * kv_);
+    small_.alloc(4 * 64 * 64 + 64);
+    status_d_ = dev_alloc<int>(ncols_);
+    clamp_d_ = dev_alloc<int>(ncols_);
+    colmask_d_ = dev_alloc<int>(ncols_);
+    jobs_d_ = dev_alloc<IterJob>(ncols_);
+    jobs_h_ = pinned<IterJob>(ncols_);
+    colmask_h_ = pinned<int>(ncols_);
+    sig_h_ = pinned<double>(std::max(ncols_, cap_));
+    status_h_ = pinned<int>(ncols_);
+    clamp_h_ = pinned<int>(ncols_);
+    stage_rows_ = 4096;
+    nrm_.alloc(stage_rows_);
+    bad_d_ = dev_alloc<int>(stage_rows_);
+    nrm_h_ = pinned<double>(stage_rows_);
+    bad_h_ = pinned<int>(stage_rows_);
+}
+
+cudaEvent_t Sketch::ev_at(size_t i) {
+    while (ev_pool_.size() <= i) {
+        cudaEvent_t e;
+        AERO_CUDA(cudaEventCreate(&e));
+        ev_pool_.push_back(e);
+    }
+    return ev_pool_[i];
+}
+
+Sketch::~Sketch() {
+    cudaSetDevice(dev_);
+    if (st_) cudaStreamSynchronize(st_);
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    for (Chunk* c : chunks_) {
+        cudaFree(c->z);
+        cudaFree(c->mt);
+        delete c;
+    }
+    cudaFree(status_d_);
+    cudaFree(clamp_d_);
+    cudaFree(colmask_d_);
+    cudaFree(jobs_d_);
+    cudaFree(bad_d_);
+    cudaFreeHost(jobs_h_);
+    cudaFreeHost(colmask_h_);
+    cudaFreeHost(sig_h_);
+    cudaFreeHost(status_h_);
+    cudaFreeHost(clamp_h_);
+    cudaFreeHost(nrm_h_);
+    cudaFreeHost(bad_h_);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+void Sketch::set_theta(double th) {  // sketch.cpp:33-36
+    if (th < 0.0) throw InvalidInput("AeroState: theta must be >= 0");
+    theta_ = th;
+}
+
+uint64_t Sketch::fork_state0(uint64_t n) const {
+    return rng_state0(seed_, fork_stream(stream_, n));
+}
+
+void Sketch::synchronize() { AERO_CUDA(cudaStreamSynchronize(st_)); }
+
+// ---------------------------------------------------------------- arena
+Chunk* Sketch::arena_alloc(int xi, int* col) {
+    if (chunks_.empty() || chunks_.back()->used + xi > chunks_.back()->cap) {
+        Chunk* c = new Chunk;
+        c->cap = std::max(xi, std::max(64, (int)std::min<int64_t>(1024, (int64_t)(1 << 24) / d_)));
+        AERO_CUDA(cudaMalloc(&c->z, sizeof(double) * (size_t)d_ * c->cap));
+        AERO_CUDA(cudaMalloc(&c->mt, sizeof(double) * (size_t)d_ * c->cap));
+        chunks_.push_back(c);
+    }
+    Chunk* c = chunks_.back();
+    *col = c->used;
+    c->used += xi;
+    c->live += xi;
+    return c;
+}
+void Sketch::arena_release(const SnapRec& s) {
+    s.chunk->live -= s.xi;
+    while (!chunks_.empty() && chunks_.front()->live == 0 && chunks_.front() != chunks_.back()) {
+        Chunk* c = chunks_.front();
+        AERO_CUDA(cudaStreamSynchronize(st_));
+        cudaFree(c->z);
+        cudaFree(c->mt);
+        delete c;
+        chunks_.pop_front();
+    }
+}
+
+// ---------------------------------------------------------------- append
+// C'[:, r..r+B) <- rows; G[0:r+B, r:r+B] = C'^T C'_new; symmetric fill
+void Sketch::append_rows(const double* dev_rows, int64_t B) {
+    const int r0 = r_;
+    AERO_CUDA(cudaMemcpyAsync(C_.p + (size_t)r0 * d_, dev_rows, sizeof(double) * d_ * B,
+                              cudaMemcpyDeviceToDevice, st_));
+    dgemm(st_, true, false, r0 + (int)B, (int)B, d_, 1.0, C_.p, d_, C_.p + (size_t)r0 * d_, d_,
+          0.0, G_.p + (size_t)r0 * cap_, cap_);
+    if (r0 > 0) {
+        const int64_t tot = (int64_t)r0 * B;
+        k_sym_fill<<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(r0, (int)B, G_.p, cap_);
+        AERO_LAUNCHED();
+    }
+}
+
+// ---------------------------------------------------------------- reduce
+// FD reduce of the full 2ell x d buffer (fd.cpp:13-29 via sketch.cpp:92-95):
+// eig(C'C'^T) = U diag(sigma^2) U^T; new rows sqrt(sigma_i^2 - sigma_ell^2) v_i^T
+// = (w_i u_i^T) C' with w_i = sqrt(s2_i)/sigma_i; keep max(ell-1, 1) rows.
+void Sketch::reduce() {
+    if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
+    const int n = cap_;
+    const int keep = std::max(ell_ - 1, 1);
+    E_.alloc((size_t)n * n);
+    ew_.alloc(n);
+    fw_.alloc(n);
+    copy_matrix(st_, n, n, G_.p, cap_, E_.p, n);
+    eigh(st_, n, E_.p, n, ew_.p);
+    fd_weights(st_, ew_.p, n, ell_, keep, fw_.p);
+    scale_columns(st_, n, keep, E_.p, n, fw_.p);
+    dgemm(st_, false, false, d_, keep, n, 1.0, C_.p, d_, E_.p, n, 0.0, C2_.p, d_);
+    std::swap(C_.p, C2_.p);
+    std::swap(C_.n, C2_.n);
+    dgemm(st_, true, false, keep, keep, d_, 1.0, C_.p, d_, C_.p, d_, 0.0, G_.p, cap_);
+    r_ = keep;
+    if (profiling) {
+        AERO_CUDA(cudaEventRecord(ev_at(1), st_));
+        AERO_CUDA(cudaEventSynchronize(ev_at(1)));
+        float ms = 0.f;
+        AERO_CUDA(cudaEventElapsedTime(&ms, ev_at(0), ev_at(1)));
+        prof.reduce_ms += ms;
+        prof.reduces++;
+    }
+}
+
+// ---------------------------------------------------------------- iterate
+void Sketch::run_iterate(int njobs, int R, int max_k) {
+    int maxphase = 0, ncol_total = 0;
+    for (int j = 0; j < njobs; ++j) {
+        maxphase = std::max(maxphase, jobs_h_[j].nphase);
+        ncol_total = std::max(ncol_total, jobs_h_[j].col + jobs_h_[j].k);
+    }
+    AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob) * njobs, cudaMemcpyHostToDevice, st_));
+    AERO_CUDA(cudaMemcpyAsync(colmask_d_, colmask_h_, sizeof(int) * ncol_total,
+                              cudaMemcpyHostToDevice, st_));
+    if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
+    iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+    for (int p = 0; p < maxphase; ++p) {
+        int ncol = 0;
+        double flops = 0.0;
+        for (int j = 0; j < njobs; ++j)
+            if (jobs_h_[j].nphase > p) {
+                ncol = std::max(ncol, jobs_h_[j].col + jobs_h_[j].k);
+                flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
+            }
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2 + 2 * p), st_));
+        dgemm(st_, false, false, R, ncol, R, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_,
+              colmask_d_);
+        if (profiling) {
+            AERO_CUDA(cudaEventRecord(ev_at(3 + 2 * p), st_));
+            prof.product_launches++;
+            prof.product_flops += flops;
+            prof.product_bytes += 8.0 * ((double)R * R + 2.0 * (double)R * ncol);
+        }
+        iter_normalize(st_, jobs_d_, njobs, p, X_.p, Y_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p,
+                       kv_, clamp_d_, std::max(max_k, 1));
+    }
+    if (profiling) AERO_CUDA(cudaEventRecord(ev_at(1), st_));
+    AERO_CUDA(cudaMemcpyAsync(sig_h_, sig_.p, sizeof(double) * ncol_total, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaMemcpyAsync(status_h_, status_d_, sizeof(int) * njobs, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaMemcpyAsync(clamp_h_, clamp_d_, sizeof(int) * njobs, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));
+    if (profiling) {
+        float ms = 0.f;
+        AERO_CUDA(cudaEventElapsedTime(&ms, ev_at(0), ev_at(1)));
+        prof.iterate_ms += ms;
+        for (int p = 0; p < maxphase; ++p) {
+            AERO_CUDA(cudaEventElapsedTime(&ms, ev_at(2 + 2 * p), ev_at(3 + 2 * p)));
+            prof.product_ms += ms;
+        }
+    }
+}
+
+// simul_iter with k > 64 columns: same r-space iteration, host-driven phases
+// with device GEMMs and the general eigensolver for the k x k Grams.
+void Sketch::run_simul_large(int k, uint64_t rng0, int r) {
+    const size_t kk = (size_t)k * k;
+    qw_.alloc(3 * kk + 3 * (size_t)k);
+    double* S = qw_.p;
+    double* Tm = S + kk;
+    double* lam = Tm + kk;
+    double* sc = lam + k;
+    if (vr_.n < kk) vr_.alloc(kk);
+    jobs_h_[0] = IterJob{1, r, k, 0, q_ + 1, 0, rng0};
+    for (int c = 0; c < k; ++c) colmask_h_[c] = r;
+    if (k > ncols_) throw InvalidInput("simul_iter: k exceeds work capacity");
+    AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob), cudaMemcpyHostToDevice, st_));
+    AERO_CUDA(cudaMemcpyAsync(colmask_d_, colmask_h_, sizeof(int) * k, cudaMemcpyHostToDevice, st_));
+    iter_init(st_, jobs_d_, 1, G_.p, cap_, X_.p, ldx_, r, status_d_);
+    AERO_CUDA(cudaMemcpyAsync(status_h_, status_d_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));
+    if (status_h_[0] != JOB_ACTIVE) {
+        for (int a = 0; a < k; ++a) sig_h_[a] = 0.0;
+        return;
+    }
+    for (int p = 0; p <= q_; ++p) {
+        dgemm(st_, false, false, r, k, r, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_, colmask_d_);
+        dgemm(st_, true, false, k, k, r, 1.0, X_.p, ldx_, Y_.p, ldx_, 0.0, S, k);
+        eigh(st_, k, S, k, lam);
+        k_inv_sqrt_clamp<<<1, 1, 0, st_>>>(lam, k, sc);
+        AERO_LAUNCHED();
+        scale_columns(st_, k, k, S, k, sc);  // T = W diag(lam^-1/2)
+        if (p == q_) dgemm(st_, false, false, r, k, k, 1.0, X_.p, ldx_, S, k, 0.0, H_.p, ldx_);
+        dgemm(st_, false, false, r, k, k, 1.0, Y_.p, ldx_, S, k, 0.0, X_.p, ldx_);
+    }
+    dgemm(st_, true, false, k, k, r, 1.0, X_.p, ldx_, X_.p, ldx_, 0.0, vr_.p, k);
+    eigh(st_, k, vr_.p, k, lam);
+    k_sqrt_clamp<<<(k + 127) / 128, 128, 0, st_>>>(lam, k, sig_.p);
+    AERO_LAUNCHED();
+    AERO_CUDA(cudaMemcpyAsync(sig_h_, sig_.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));
+}
+
+// ---------------------------------------------------------------- dump
+// sketch.cpp:119-132: z = g V[:, :xi] = C'^T (H V); sign fix (linalg.cpp:150);
+// m = (C'z)^T C'; C <- C' - (C'z) z^T; G <- G - 2PP^T + P (z^T z) P^T, P = C'z
+void Sketch::dump_from_job(int col, int k, int xi, int64_t t, double theta, bool zero_buffer) {
+    int ccol = 0;
+    Chunk* ch = arena_alloc(xi, &ccol);
+    double* z = ch->z + (size_t)ccol * d_;
+    double* mt = ch->mt + (size_t)ccol * d_;
+    const int r = r_;
+    if (zero_buffer) {  // linalg.cpp:132-135: z = I(d, k), C' = 0 so m = 0
+        const int64_t tot = (int64_t)d_ * xi;
+        k_identity_cols<<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(d_, xi, z, d_);
+        AERO_LAUNCHED();
+        fill_zero(st_, mt, tot);
+    } else {
+        qy_.alloc((size_t)r * xi * 2 + (size_t)xi * xi + 64);
+        double* HV = qy_.p;
+        double* P = HV + (size_t)r * xi;
+        double* ZZ = P + (size_t)r * xi;
+        const double* vr = (k > 64) ? vr_.p : vr_.p + (size_t)col * kv_;
+        dgemm(st_, false, false, r, xi, k, 1.0, H_.p + (size_t)col * ldx_, ldx_, vr, k, 0.0, HV, r);
+        dgemm(st_, false, false, d_, xi, r, 1.0, C_.p, d_, HV, r, 0.0, z, d_);
+        fix_column_signs(st_, d_, xi, z, d_, nullptr);
+        dgemm(st_, true, false, r, xi, d_, 1.0, C_.p, d_, z, d_, 0.0, P, r);      // P = C' z
+        dgemm(st_, false, false, d_, xi, r, 1.0, C_.p, d_, P, r, 0.0, mt, d_);     // m^T = C'^T P
+        dgemm(st_, false, true, d_, r, xi, -1.0, z, d_, P, r, 1.0, C_.p, d_);      // C' -= P z^T
+        dgemm(st_, true, false, xi, xi, d_, 1.0, z, d_, z, d_, 0.0, ZZ, xi);       // z^T z
+        add_identity(st_, xi, ZZ, xi, -2.0);
+        dgemm(st_, false, false, r, xi, xi, 1.0, P, r, ZZ, xi, 0.0, HV, r);        // P (z^T z - 2I)
+        dgemm(st_, false, true, r, r, xi, 1.0, HV, r, P, r, 1.0, G_.p, cap_);
+        symmetrize(st_, r, G_.p, cap_);
+    }
+    SnapRec s{xi, last_dump_t_ + 1, t, theta, ch, ccol};
+    last_dump_t_ = t;
+    snaps_.push_back(s);
+}
+
+// ---------------------------------------------------------------- doubling
+// sketch.cpp:108-139 for one row, starting at rank k (forks consumed so far
+// are already in forks_)
+void Sketch::doubling(int k, int64_t t, double theta, aero_event* ev) {
+    const int kmax = std::min({ell_, d_, r_});
+    while (true) {
+        ev->doubling_steps++;
+        ev->simul_calls++;
+        const uint64_t f = ++forks_;
+        bool zero = false;
+        if (k <= 64) {
+            jobs_h_[0] = IterJob{1, r_, k, 0, q_ + 1, 0, fork_state0(f)};
+            for (int c = 0; c < k; ++c) colmask_h_[c] = r_;
+            run_iterate(1, r_, k);
+            zero = status_h_[0] == JOB_ZERO;
+        } else {
+            run_simul_large(k, fork_state0(f), r_);
+            zero = status_h_[0] != JOB_ACTIVE;
+        }
+        const double tail = sig_h_[k - 1] * sig_h_[k - 1];
+        ev->k_last = k;
+        ev->tail_sq = tail;
+        if (tail < theta || k == kmax) {
+            int xi = 0;
+            for (int j = 0; j < k; ++j) {
+                if (sig_h_[j] * sig_h_[j] >= theta) xi = j + 1;
+                else break;
+            }
+            ev->xi = xi;
+            if (xi >= 1) {
+                dump_from_job(0, k, xi, t, theta, zero);
+                ev->dumped = 1;
+            }
+            break;
+        }
+        k = std::min(2 * k, kmax);
+    }
+}
+
+// ---------------------------------------------------------------- single row
+void Sketch::single_row(const double* dev_row, int64_t t, double theta, aero_event* ev) {
+    ev->forks_before = (int64_t)forks_;
+    append_rows(dev_row, 1);
+    r_ += 1;
+    if (r_ == cap_) {
+        reduce();
+        ev->reduced = 1;
+    }
+    const uint64_t f = ++forks_;
+    jobs_h_[0] = IterJob{0, r_, 1, 0, kp_ + 1, 0, fork_state0(f)};
+    colmask_h_[0] = r_;
+    run_iterate(1, r_, 1);
+    const double s1 = (status_h_[0] == JOB_ACTIVE) ? sig_h_[0] : 0.0;
+    ev->sigma1_sq = s1;
+    if (s1 >= 0.5 * theta) {  // sketch.cpp:100
+        ev->gate_fired = 1;
+        doubling(std::min(2, std::min({ell_, d_, r_})), t, theta, ev);
+    }
+    clock_ = t;
+    ev->forks_after = (int64_t)forks_;
+    ev->rows_after = r_;
+}
+
+// ---------------------------------------------------------------- batch
+// Speculative batch of B rows (no reduce inside): every row's gate (and, under
+// the FIRE1 pattern, its first doubling step at k = min(2, kmax)) is computed
+// at once on the masked prefix of the batch-final Gram; rows are then
+// validated in order and the first row whose outcome differs from the
+// prediction (or that dumps) ends the batch. Returns rows consumed (>= 1).
+int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
+                          const double* thetas, aero_event* log) {
+    const int r0 = r_;
+    const uint64_t F = forks_;
+    const Pattern pat = pattern_;
+    append_rows(dev_rows, B);
+    const int R = r0 + (int)B;
+    int njobs = 0;
+    const int gate_base = (pat == FIRE1) ? 2 * (int)B : 0;
+    if (pat == FIRE1) {
+        for (int j = 0; j < B; ++j) {
+            const int rj = r0 + j + 1;
+            const int kj = std::min(2, std::min({ell_, d_, rj}));
+            jobs_h_[njobs++] = IterJob{1, rj, kj, 2 * j, q_ + 1, 0, fork_state0(F + 2 * j + 2)};
+            colmask_h_[2 * j] = rj;
+            colmask_h_[2 * j + 1] = (kj == 2) ? rj : 0;
+        }
+    }
+    for (int j = 0; j < B; ++j) {
+        const int rj = r0 + j + 1;
+        const uint64_t gf = (pat == FIRE1) ? F + 2 * j + 1 : F + j + 1;
+        jobs_h_[njobs++] = IterJob{0, rj, 1, gate_base + j, kp_ + 1, 0, fork_state0(gf)};
+        colmask_h_[gate_base + j] = rj;
+    }
+    run_iterate(njobs, R, 2);
+    batches++;
+    const int simul_job0 = 0, gate_job0 = (pat == FIRE1) ? (int)B : 0;
+    uint64_t forks = F;
+    for (int64_t j = 0; j < B; ++j) {
+        aero_event* ev = log + j;
+        *ev = aero_event{};
+        ev->t = t[j];
+        ev->theta = thetas[j];
+        ev->forks_before = (int64_t)forks;
+        const double theta = thetas[j];
+        const int gj = gate_job0 + (int)j;
+        const double s1 = (status_h_[gj] == JOB_ACTIVE) ? sig_h_[gate_base + j] : 0.0;
+        ev->sigma1_sq = s1;
+        const bool fire = s1 >= 0.5 * theta;
+        const int rj = r0 + (int)j + 1;
+        auto commit = [&]() {
+            r_ = rj;
+            clock_ = t[j];
+            ev->forks_after = (int64_t)forks_;
+            ev->rows_after = r_;
+            theta_ = theta;
+            rows_processed++;
+        };
+        if (pat == NOFIRE) {
+            forks = F + j + 1;
+            forks_ = forks;
+            if (fire) {  // mispredicted: finish this row exactly, drop the rest
+                r_ = rj;
+                ev->gate_fired = 1;
+                doubling(std::min(2, std::min({ell_, d_, rj})), t[j], theta, ev);
+                commit();
+                pattern_ = FIRE1;
+                mispredicts++;
+                return j + 1;
+            }
+            commit();
+            continue;
+        }
+        // FIRE1
+        forks = F + 2 * j + 1;
+        forks_ = forks;
+        if (!fire) {
+            commit();
+            pattern_ = NOFIRE;
+            mispredicts++;
+            return j + 1;
+        }
+        ev->gate_fired = 1;
+        ev->doubling_steps = 1;
+        ev->simul_calls = 1;
+        forks = F + 2 * j + 2;
+        forks_ = forks;
+        const int kmax = std::min({ell_, d_, rj});
+        const int k = std::min(2, kmax);
+        const int sj = simul_job0 + (int)j;
+        const double* sg = sig_h_ + 2 * j;
+        const bool zero = status_h_[sj] == JOB_ZERO;
+        const double tail = sg[k - 1] * sg[k - 1];
+        ev->k_last = k;
+        ev->tail_sq = tail;
+        if (tail < theta || k == kmax) {
+            int xi = 0;
+            for (int a = 0; a < k; ++a) {
+                if (sg[a] * sg[a] >= theta) xi = a + 1;
+                else break;
+            }
+            ev->xi = xi;
+            if (xi >= 1) {  // state changes: dump, end the batch after this row
+                r_ = rj;
+                dump_from_job(2 * (int)j, k, xi, t[j], theta, zero);
+                ev->dumped = 1;
+                commit();
+                pattern_ = FIRE1;
+                if (j + 1 < B) mispredicts++;
+                return j + 1;
+            }
+            commit();
+            continue;
+        }
+        // needs a larger rank: continue the doubling for this row exactly
+        r_ = rj;
+        doubling(std::min(2 * k, kmax), t[j], theta, ev);
+        commit();
+        pattern_ = FIRE1;
+        mispredicts++;
+        return j + 1;
+    }
+    pattern_ = pat;
+    return B;
+}
+
+void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
+                          const double* thetas, aero_event* log) {
+    int64_t pos = 0;
+    while (pos < n) {
+        const int64_t room = (int64_t)cap_ - 1 - r_;  // rows that fit before a reduce
+        if (exact_ || room < 2 || n - pos < 2) {
+            aero_event* ev = log + pos;
+            *ev = aero_event{};
+            ev->t = t[pos];
+            ev->theta = thetas[pos];
+            theta_ = thetas[pos];
+            single_row(dev_rows + (size_t)pos * d_, t[pos], thetas[pos], ev);
+            rows_processed++;
+            pos++;
+            continue;
+        }
+        const int64_t B = std::min<int64_t>({(int64_t)max_batch_, n - pos, room});
+        pos += run_batch(dev_rows + (size_t)pos * d_, B, t + pos, thetas + pos, log + pos);
+    }
+    if (n > 0) last_ev_ = log[n - 1];
+}
+
+// ---------------------------------------------------------------- update
+void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t,
+                          const double* theta_per_row, aero_event* log) {
+    if (n <= 0) return;
+    if (ld < d_) throw InvalidInput("AeroState: row dimension mismatch");
+    AERO_CUDA(cudaSetDevice(dev_));
+    std::vector<aero_event> local;
+    if (!log) {
+        local.resize(n);
+        log = local.data();
+    }
+    std::vector<double> th;
+    for (int64_t off = 0; off < n; off += stage_rows_) {
+        const int64_t cnt = std::min<int64_t>(stage_rows_, n - off);
+        stage_.alloc((size_t)stage_rows_ * d_);
+        // stage rows contiguously (ld = d) on the device
+        AERO_CUDA(cudaMemcpy2DAsync(stage_.p, sizeof(double) * d_, rows + off * ld,
+                                    sizeof(double) * ld, sizeof(double) * d_, cnt,
+                                    device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                    st_));
+        ingest_rows(st_, stage_.p, cnt, d_, d_, nrm_.p, bad_d_);
+        AERO_CUDA(cudaMemcpyAsync(nrm_h_, nrm_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+        AERO_CUDA(cudaMemcpyAsync(bad_h_, bad_d_, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st_));
+        AERO_CUDA(cudaStreamSynchronize(st_));
+        // validation in row order (sketch.cpp:83-85): the first offending row
+        // raises after the rows before it were absorbed
+        int64_t good = cnt;
+        std::string err;
+        int64_t prev = (off == 0) ? clock_ : t[off - 1];
+        for (int64_t j = 0; j < cnt; ++j) {
+            if (bad_h_[j]) { good = j; err = "AeroState: non-finite row"; break; }
+            if (t[off + j] <= prev) { good = j; err = "AeroState: timestamp regression"; break; }
+            prev = t[off + j];
+        }
+        th.resize(good);
+        for (int64_t j = 0; j < good; ++j) {
+            if (mode_ == AERO_THETA_ATTP) {  // attp.hpp:22-23
+                fro_mass_ += nrm_h_[j];
+                th[j] = eps_ * fro_mass_;
+            } else if (theta_per_row) {
+                if (theta_per_row[off + j] < 0.0) throw InvalidInput("AeroState: theta must be >= 0");
+                th[j] = theta_per_row[off + j];
+            } else {
+                th[j] = theta_;
+            }
+        }
+        process_rows(stage_.p, good, t + off, th.data(), log + off);
+        if (good < cnt) throw InvalidInput(err);
+    }
+}
+
+// ---------------------------------------------------------------- queries
+void Sketch::ensure_query_buffers() {
+    Bq_.alloc((size_t)d_ * d_);
+    Wq_.alloc((size_t)d_ * d_ + d_);
+}
+
+void Sketch::accumulate_residual(double* B, double beta_first) {
+    if (r_ > 0)
+        dgemm(st_, false, true, d_, d_, r_, 1.0, C_.p, d_, C_.p, d_, beta_first, B, d_);
+    else if (beta_first == 0.0)
+        fill_zero(st_, B, (int64_t)d_ * d_);
+}
+
+// sketch.cpp:162-165 summed over snaps [first, last): B += Z M + (Z M)^T - Z (M Z) Z^T
+void Sketch::accumulate_restore(double* B, int64_t first, int64_t last) {
+    int64_t i = first;
+    std::vector<int> offs, wids;
+    while (i < last) {
+        const Chunk* ch = snaps_[i].chunk;
+        const int c0 = snaps_[i].col;
+        int64_t j = i;
+        int cols = 0;
+        offs.clear();
+        wids.clear();
+        while (j < last && snaps_[j].chunk == ch && snaps_[j].col == c0 + cols) {
+            offs.push_back(snaps_[j].col);
+            wids.push_back(snaps_[j].xi);
+            cols += snaps_[j].xi;
+            ++j;
+        }
+        const double* Z = ch->z + (size_t)c0 * d_;
+        const double* Mt = ch->mt + (size_t)c0 * d_;
+        dgemm(st_, false, true, d_, d_, cols, 1.0, Z, d_, Mt, d_, 1.0, B, d_);  // Z M
+        dgemm(st_, false, true, d_, d_, cols, 1.0, Mt, d_, Z, d_, 1.0, B, d_);  // (Z M)^T
+        qy_.alloc((size_t)d_ * ch->cap + 2 * (size_t)ch->cap + 64);
+        double* Yk = qy_.p;
+        // per-snapshot K terms (batched kernel for xi <= 64, GEMMs otherwise)
+        std::vector<int> so, sw;
+        for (size_t s = 0; s < offs.size(); ++s) {
+            if (wids[s] <= 64) {
+                so.push_back(offs[s]);
+                sw.push_back(wids[s]);
+            } else {
+                const int xi = wids[s];
+                double* zs = ch->z + (size_t)offs[s] * d_;
+                double* ms = ch->mt + (size_t)offs[s] * d_;
+                qw_.alloc((size_t)xi * xi);
+                dgemm(st_, true, false, xi, xi, d_, 1.0, ms, d_, zs, d_, 0.0, qw_.p, xi);
+                dgemm(st_, false, false, d_, xi, xi, 1.0, zs, d_, qw_.p, xi, 0.0,
+                      Yk + (size_t)offs[s] * d_, d_);
+            }
+        }
+        if (!so.empty()) {
+            int* dso = nullptr;
+            AERO_CUDA(cudaMallocAsync(&dso, sizeof(int) * 2 * so.size(), st_));
+            AERO_CUDA(cudaMemcpyAsync(dso, so.data(), sizeof(int) * so.size(), cudaMemcpyHostToDevice, st_));
+            AERO_CUDA(cudaMemcpyAsync(dso + so.size(), sw.data(), sizeof(int) * sw.size(),
+                                      cudaMemcpyHostToDevice, st_));
+            restore_k_terms(st_, d_, ch->z, ch->mt, d_, dso, dso + so.size(), (int)so.size(), Yk);
+            AERO_CUDA(cudaFreeAsync(dso, st_));
+            AERO_CUDA(cudaStreamSynchronize(st_));
+        }
+        dgemm(st_, false, true, d_, d_, cols, -1.0, Yk + (size_t)c0 * d_, d_, Z, d_, 1.0, B, d_);
+        i = j;
+    }
+}
+
+const double* Sketch::query_gram_device(int64_t lb, int64_t ub) {
+    if (lb >= ub) throw InvalidInput("AeroState: query needs lb < ub");
+    if (ub > clock_) throw InvalidInput("AeroState: query beyond clock");
+    AERO_CUDA(cudaSetDevice(dev_));
+    ensure_query_buffers();
+    fill_zero(st_, Bq_.p, (int64_t)d_ * d_);
+    if (ub == clock_ && r_ > 0) accumulate_residual(Bq_.p, 0.0);  // sketch.cpp:150
+    // first snapshot with t > lb (sketch.cpp:153-157), then while t <= ub
+    int64_t first = 0, last = 0;
+    while (first < (int64_t)snaps_.size() && snaps_[first].t <= lb) ++first;
+    last = first;
+    while (last < (int64_t)snaps_.size() && snaps_[last].t <= ub) ++last;
+    accumulate_restore(Bq_.p, first, last);
+    return Bq_.p;
+}
+
+void Sketch::query_gram(int64_t lb, int64_t ub, double* out_host) {
+    const double* B = query_gram_device(lb, ub);
+    AERO_CUDA(cudaMemcpyAsync(out_host, B, sizeof(double) * d_ * d_, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));  // symmetric: column-major == row-major
+}
+
+// shrink_to_sketch (sketch.cpp:167-178)
+void Sketch::query(int64_t lb, int64_t ub, double* out_host) {
+    const double* B = query_gram_device(lb, ub);
+    copy_matrix(st_, d_, d_, B, d_, Wq_.p, d_);
+    double* w = Wq_.p + (size_t)d_ * d_;
+    eigh(st_, d_, Wq_.p, d_, w);
+    qy_.alloc((size_t)ell_ * d_);
+    shrink_rows(st_, w, Wq_.p, d_, d_, ell_, qy_.p);
+    AERO_CUDA(cudaMemcpyAsync(out_host, qy_.p, sizeof(double) * ell_ * d_, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Sketch::residual(double* out, int64_t max_rows) {
+    const int64_t rows = std::min<int64_t>(r_, max_rows);
+    AERO_CUDA(cudaMemcpyAsync(out, C_.p, sizeof(double) * d_ * rows, cudaMemcpyDeviceToHost, st_));
+    AERO_CUDA(cudaStreamSynchronize(st_));
+}
+
+const SnapRec& Sketch::snap(int64_t i) const {
+    if (i < 0 || i >= (int64_t)snaps_.size()) throw InvalidInput("snapshot index out of range");
+    return snaps_[i];
+}
+void Sketch::snap_get(int64_t i, double* z, double* m) {
+    const SnapRec& s = snap(i);
+    if (z) {  // device z is d x xi column-major; the ABI wants d x xi row-major
+        std::vector<double> tmp((size_t)d_ * s.xi);
+        AERO_CUDA(cudaMemcpyAsync(tmp.data(), s.chunk->z + (size_t)s.col * d_,
+                                  sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, st_));
+        AERO_CUDA(cudaStreamSynchronize(st_));
+        for (int j = 0; j < s.xi; ++j)
+            for (int i2 = 0; i2 < d_; ++i2) z[(size_t)i2 * s.xi + j] = tmp[(size_t)j * d_ + i2];
+    }
+    if (m) {  // m^T column-major d x xi == m row-major xi x d
+        AERO_CUDA(cudaMemcpyAsync(m, s.chunk->mt + (size_t)s.col * d_,
+                                  sizeof(double) * (size_t)d_ * s.xi, cudaMemcpyDeviceToHost, st_));
+        AERO_CUDA(cudaStreamSynchronize(st_));
+    }
+}
+void Sketch::snap_pop_front() {
+    if (snaps_.empty()) return;
+    const SnapRec s = snaps_.front();
+    snaps_.pop_front();
+    arena_release(s);
+}
+
+void Sketch::info(aero_info* o) const {
+    o->d = d_;
+    o->ell = ell_;
+    o->rows = r_;
+    o->clock = clock_;
+    o->last_dump_t = last_dump_t_;
+    o->forks = (int64_t)forks_;
+    o->snaps = (int64_t)snaps_.size();
+    int64_t cols = 0;
+    for (const SnapRec& s : snaps_) cols += s.xi;
+    o->snap_cols = cols;
+    o->theta = theta_;
+    o->fro_mass = fro_mass_;
+    o->device_rows_processed = rows_processed;
+    o->device_batches = batches;
+    o->device_mispredicts = mispredicts;
+}
+
+}  // namespace aero_b200

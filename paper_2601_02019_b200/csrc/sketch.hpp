@@ -1,0 +1,144 @@
+// Host-side engine of one AeroState on a B200: device-resident buffer C'
+// (d x 2ell, column-major == reference row-major rows), its Gram G = C'C'^T
+// (2ell x 2ell), snapshot arena; host-side control mirrors
+// /root/reference/proj/src/sketch.cpp:82-141 with speculative row batching.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/aero_b200.h"
+#include "kernels.cuh"
+
+namespace aero_b200 {
+
+struct Chunk {
+    double* z = nullptr;   // d x cap (column-major): snapshot directions
+    double* mt = nullptr;  // d x cap: m^T of each snapshot (m = (C'z)^T C')
+    int cap = 0, used = 0, live = 0;
+};
+struct SnapRec {
+    int xi;
+    int64_t s, t;
+    double theta;
+    Chunk* chunk;
+    int col;
+};
+
+struct DeviceBuf {  // RAII device allocation
+    double* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count);
+    void release();
+    ~DeviceBuf() { release(); }
+};
+
+class Sketch {
+  public:
+    explicit Sketch(const aero_cfg& cfg);
+    ~Sketch();
+    Sketch(const Sketch&) = delete;
+    Sketch& operator=(const Sketch&) = delete;
+
+    void set_theta(double th);
+    // rows: host or device pointer (row-major, ld); n sequential updates
+    void update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t,
+                      const double* theta_per_row, aero_event* log);
+    // restored Gram (sketch.cpp:146-159) into device d x d buffer; returns ptr
+    const double* query_gram_device(int64_t lb, int64_t ub);
+    void query(int64_t lb, int64_t ub, double* out_host);       // ell x d
+    void query_gram(int64_t lb, int64_t ub, double* out_host);  // d x d
+    void residual(double* out, int64_t max_rows);
+    int64_t snap_count() const { return (int64_t)snaps_.size(); }
+    const SnapRec& snap(int64_t i) const;
+    void snap_get(int64_t i, double* z, double* m);
+    void snap_pop_front();
+    void info(aero_info* out) const;
+    const aero_event& last_event() const { return last_ev_; }
+    void synchronize();
+
+    int d() const { return d_; }
+    int ell() const { return ell_; }
+    int rows() const { return r_; }
+    int64_t clock() const { return clock_; }
+    double theta() const { return theta_; }
+    double eps() const { return eps_; }
+    int device() const { return dev_; }
+    cudaStream_t stream() const { return st_; }
+    const double* buffer() const { return C_.p; }  // d x rows column-major
+    // snapshot device views for the coordinator / queries
+    const std::deque<SnapRec>& snaps() const { return snaps_; }
+    // add restore contributions of snaps [first, last) into device B (d x d)
+    void accumulate_restore(double* B, int64_t first, int64_t last);
+    // B += C C^T of the live residual
+    void accumulate_residual(double* B, double beta_first);
+
+    // counters
+    int64_t rows_processed = 0, batches = 0, mispredicts = 0;
+    aero_profile prof{};
+    bool profiling = false;
+
+  private:
+    enum Pattern { NOFIRE = 0, FIRE1 = 1 };
+    void process_rows(const double* dev_rows, int64_t n, const int64_t* t, const double* thetas,
+                      aero_event* log);
+    int64_t run_batch(const double* dev_rows, int64_t B, const int64_t* t, const double* thetas,
+                      aero_event* log);
+    void single_row(const double* dev_row, int64_t t, double theta, aero_event* ev);
+    void append_rows(const double* dev_rows, int64_t B);
+    void reduce();
+    // finish a row whose gate fired: doubling from k (forks already consumed up
+    // to the gate / previous steps); uses device X/H columns of a job if given
+    void doubling(int k, int64_t t, double theta, aero_event* ev);
+    void dump_from_job(int col, int k, int xi, int64_t t, double theta, bool zero_buffer);
+    // run jobs already written to jobs_h_ (njobs); results in sig_h_/status_h_/clamp_h_
+    void run_iterate(int njobs, int R, int max_k);
+    void run_simul_large(int k, uint64_t rng0, int r);
+    uint64_t fork_state0(uint64_t n) const;
+    Chunk* arena_alloc(int xi, int* col);
+    void arena_release(const SnapRec& s);
+    void ensure_query_buffers();
+
+    // config
+    int d_, ell_, cap_, kp_, q_, mode_, max_batch_;
+    bool exact_;
+    std::vector<cudaEvent_t> ev_pool_;
+    cudaEvent_t evA_ = nullptr, evB_ = nullptr;
+    cudaEvent_t ev_at(size_t i);
+    double eps_, eps_si_;
+    uint64_t seed_, stream_;
+    int dev_;
+    cudaStream_t st_ = nullptr;
+    // host state
+    double theta_, fro_mass_ = 0.0;
+    int64_t clock_ = 0, last_dump_t_ = 0;
+    uint64_t forks_ = 0;
+    int r_ = 0;
+    Pattern pattern_ = FIRE1;
+    std::deque<SnapRec> snaps_;
+    std::deque<Chunk*> chunks_;
+    aero_event last_ev_{};
+    // device buffers
+    DeviceBuf C_, C2_, G_, E_, ew_, fw_, stage_, nrm_, X_, Y_, H_, sig_, vr_, small_, Bq_, Wq_,
+        qw_, qy_;
+    int* status_d_ = nullptr;
+    int* clamp_d_ = nullptr;
+    int* colmask_d_ = nullptr;
+    int* bad_d_ = nullptr;
+    IterJob* jobs_d_ = nullptr;
+    int ldx_ = 0, ncols_ = 0, kv_ = 64, stage_rows_ = 0;
+    // pinned host mirrors
+    IterJob* jobs_h_ = nullptr;
+    int* colmask_h_ = nullptr;
+    double* sig_h_ = nullptr;
+    int* status_h_ = nullptr;
+    int* clamp_h_ = nullptr;
+    double* nrm_h_ = nullptr;
+    int* bad_h_ = nullptr;
+};
+
+}  // namespace aero_b200

@@ -1,0 +1,313 @@
+"""GPU parity tests: the product path (C-ABI -> sm_100a kernels) against the
+CPU oracle on the same seeded inputs. Known-answer tests are the reference's
+own (proj/tests/test_sketch.cpp, test_attp.cpp, test_sliding_window.cpp,
+test_distributed.cpp); the stream tests use the BASELINE configs' generator
+at sizes the oracle finishes in seconds.
+
+Tolerances (fp64 on both sides, different summation orders):
+  * decision trace (gate, reduce, dump, xi, doubling steps, fork counters,
+    rows): bit-exact
+  * sigma estimates: relative 1e-8
+  * restored Gram B^T B: relative Frobenius 1e-9
+  * covariance error: <= eps and |err_gpu - err_oracle| <= 1e-6
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_2601_02019_b200 as prod  # noqa: E402
+from refutil import gaussian, gaussian_vec, orthonormal, uniform_rows  # noqa: E402
+
+TRACE_FIELDS = ("t", "forks_before", "forks_after", "rows_after", "reduced", "gate_fired", "dumped",
+                "doubling_steps", "simul_calls", "xi", "k_last")
+
+
+def assert_trace_equal(ev_gpu, ev_ref, rtol=1e-8):
+    for f in TRACE_FIELDS:
+        bad = np.nonzero(ev_gpu[f] != ev_ref[f])[0]
+        assert bad.size == 0, (f, bad[:5], ev_gpu[f][bad[:5]], ev_ref[f][bad[:5]])
+    for f in ("sigma1_sq", "tail_sq", "theta"):
+        a, b = ev_gpu[f], ev_ref[f]
+        den = np.maximum(np.abs(b), 1e-300)
+        rel = np.abs(a - b) / den
+        assert np.all((rel <= rtol) | (np.abs(a - b) < 1e-12)), (f, np.max(rel), np.argmax(rel))
+
+
+def rel_fro(a, b):
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / den if den > 0 else np.linalg.norm(a - b)
+
+
+# ---------------------------------------------------------------- rng
+def test_device_rng_matches_reference_draws(orc):
+    for seed, stream, fork, n in ((1, 1000, 1, 9), (1, 1000, 2, 1000), (7, 3, 5, 257), (0, 0, 0, 64)):
+        ref = orc.rng_draw(seed, stream, fork, n)
+        got = prod.rng_gaussians(seed, stream, fork, n)
+        assert np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref))) < 4e-16
+
+
+# ---------------------------------------------------------------- sketch KATs
+def test_dominant_row_dumped():  # test_sketch.cpp:35-51
+    s = prod.AeroState(2, 1.0, 1.0, seed=7, stream=0)
+    ev = s.update([10.0, 0.0], 1)
+    sn = s.snaps()
+    assert len(sn) == 1 and sn[0]["z"].shape[1] == 1
+    assert abs(abs(sn[0]["z"][0, 0]) - 1) < 1e-9
+    assert abs(abs(sn[0]["m"][0, 0]) - 100.0) < 1e-7 and abs(sn[0]["m"][0, 1]) < 1e-9
+    assert sn[0]["s"] == 1 and sn[0]["t"] == 1 and sn[0]["theta"] == 1.0
+    assert np.linalg.norm(s.residual()) < 1e-9 and ev["dumped"] == 1
+    b = s.query(0, 1)  # test_sketch.cpp:132-141
+    g = np.outer([10.0, 0.0], [10.0, 0.0])
+    assert np.linalg.norm(b.T @ b - g) / np.linalg.norm(g) < 1e-8
+
+
+def test_unreachable_threshold_and_reduce_once(orc):  # test_sketch.cpp:53-76
+    s = prod.AeroState(2, 1.0, 1e6, seed=7)
+    ev = s.update([1.0, 0.0], 1)
+    assert s.snap_count() == 0 and np.array_equal(s.residual()[0], [1.0, 0.0]) and ev["gate_fired"] == 0
+    s = prod.AeroState(8, 1.0, 1e9, seed=3)
+    reduces = 0
+    for i in range(1, 6):
+        a = gaussian_vec(orc, 8, 100 + i)
+        ev = s.update(a / np.linalg.norm(a), i)
+        if ev["reduced"]:
+            reduces += 1
+            assert s.residual().shape[0] <= s.ell - 1
+        assert s.residual().shape[0] <= 2 * s.ell
+    assert reduces == 1
+
+
+def test_validation_errors():  # test_sketch.cpp:19-33, 78-130
+    for args in ((4, 0.0, 0.0), (4, 1.5, 0.0), (4, 0.5, -1.0), (0, 0.5, 0.0)):
+        with pytest.raises(prod.InvalidInput):
+            prod.AeroState(*args)
+    assert prod.AeroState(4, 0.1).ell == 20 and prod.AeroState(300, 0.05).ell == 40
+    s = prod.AeroState(4, 0.5, 0.0)
+    s.update(np.ones(4), 1)
+    with pytest.raises(prod.InvalidInput):
+        s.update(np.ones(4), 1)
+    s.update(np.ones(4), 5)
+    assert s.clock == 5
+    with pytest.raises(prod.InvalidInput):
+        s.update(np.ones(3), 6)
+    bad = np.ones(4)
+    bad[2] = np.nan
+    with pytest.raises(prod.InvalidInput):
+        s.update(bad, 6)
+    for lb, ub in ((5, 5), (6, 5), (0, 6)):
+        with pytest.raises(prod.InvalidInput):
+            s.query(lb, ub)
+    z = prod.AeroState(4, 0.5, 1e9)
+    z.update(np.zeros(4), 1)
+    b = z.query(0, 1)
+    assert b.shape == (z.ell, 4) and np.linalg.norm(b) == 0.0
+
+
+def test_block_stops_at_first_bad_row():
+    s = prod.AeroState(4, 0.5, 1e9)
+    rows = np.ones((5, 4))
+    rows[3, 1] = np.inf
+    with pytest.raises(prod.InvalidInput):
+        s.update_block(rows, np.arange(1, 6))
+    assert s.clock == 3  # rows before the offending one were absorbed
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_snapshot_invariants_and_trace(orc, exact):  # test_sketch.cpp:178-204
+    rows = np.stack([gaussian_vec(orc, 8, 300, i) for i in range(1, 201)])
+    ref = orc.AeroState(8, 0.5, 5.0, 21, 0)
+    ev_ref = ref.update_block(rows, np.arange(1, 201))
+    s = prod.AeroState(8, 0.5, 5.0, seed=21, stream=0, exact=exact)
+    ev = s.update_block(rows, np.arange(1, 201))
+    assert_trace_equal(ev, ev_ref)
+    sn = s.snaps()
+    assert sn
+    prev = 0
+    for x, y in zip(sn, ref.snaps()):
+        xi = x["z"].shape[1]
+        assert np.linalg.norm(x["z"].T @ x["z"] - np.eye(xi)) < 1e-8
+        assert x["s"] == prev + 1 and x["s"] <= x["t"] and x["theta"] == 5.0
+        assert (x["s"], x["t"], xi) == (y["s"], y["t"], y["z"].shape[1])
+        assert rel_fro(x["z"] @ x["m"], y["z"] @ y["m"]) < 1e-8
+        prev = x["t"]
+    assert rel_fro(s.query_gram(0, 200), ref.query_gram(0, 200)) < 1e-9
+    g = rows.T @ rows
+    b = s.query(0, 200)
+    assert orc.spectral_norm_sym(g - b.T @ b) < np.trace(g) / 2
+
+
+def test_determinism():  # test_sketch.cpp:217-226
+    rng = np.random.default_rng(0)
+    rows = rng.standard_normal((80, 8))
+
+    def run():
+        s = prod.AeroState(8, 0.5, 3.0, seed=13, stream=4)
+        s.update_block(rows, np.arange(1, 81))
+        return s.query(0, 80)
+
+    assert np.array_equal(run(), run())
+
+
+# ---------------------------------------------------------------- attp
+def test_attp_threshold_and_persistence(orc):  # test_attp.cpp:19-83
+    s = prod.AttpState(4, 0.1)
+    s.update(np.eye(4)[0], 1)
+    assert abs(s.theta - 0.1) < 1e-12 and abs(s.fro_mass - 1.0) < 1e-12
+    s.update(2 * np.eye(4)[1], 2)
+    assert abs(s.fro_mass - 5.0) < 1e-12 and abs(s.theta - 0.5) < 1e-12
+    s = prod.AttpState(8, 0.5, seed=3)
+    rows = np.stack([gaussian_vec(orc, 8, 41, i) for i in range(1, 401)])
+    s.update_block(rows[:300], np.arange(1, 301))
+    before = [s.query(t) for t in (50, 100, 200)]
+    s.update_block(rows[300:], np.arange(301, 401))
+    for t, b in zip((50, 100, 200), before):
+        assert np.array_equal(s.query(t), b)  # historical answers bitwise stable
+    d, eps = 8, 0.25
+    s = prod.AttpState(d, eps, seed=5, stream=6)
+    rows = uniform_rows(orc, 400, d, 5, 0)
+    s.update_block(rows, np.arange(1, 401))
+    for t in (100, 200, 300, 400):
+        g = rows[:t].T @ rows[:t]
+        b = s.query(t)
+        assert orc.spectral_norm_sym(g - b.T @ b) <= eps * np.sum(rows[:t] ** 2)
+    with pytest.raises(prod.InvalidInput):
+        s.query(0)
+    with pytest.raises(prod.InvalidInput):
+        s.query(401)
+
+
+def c1_rows(orc, n, t0=1):
+    return orc.gen_rows(1024, 32, 0.9, 0.1, 64.0, 1, 0, t0, n)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_c1_trace_parity(orc, exact):
+    """Config C1 (d=1024, eps=1/16) prefix: identical decision trace, Gram
+    within 1e-9, covariance error within the budget on both sides."""
+    n = 1200 if not exact else 400
+    rows = c1_rows(orc, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(1024, 1 / 16, 1, 1000)
+    ev_ref = ref.update_block(rows, ts)
+    s = prod.AttpState(1024, 1 / 16, seed=1, stream=1000, exact=exact)
+    ev = s.update_block(rows, ts)
+    assert_trace_equal(ev, ev_ref)
+    assert ev["gate_fired"].mean() > 0.5  # the regime the bench measures
+    gq = s.query_gram(0, n)
+    gr = ref.inner.query_gram(0, n)
+    assert rel_fro(gq, gr) < 1e-9
+    g = orc.OracleGram(1024)
+    g.add_block(rows, ts)
+    e_gpu, e_ref = g.error(s.query(n)), g.error(ref.query(n))
+    assert e_gpu <= 1 / 16 and abs(e_gpu - e_ref) <= 1e-6
+
+
+def test_large_ell_path_parity(orc):
+    """ell=128 (2ell=256 > the one-CTA eigensolver): exercises the large-n
+    reduce path and batches over r in [127, 255]."""
+    d, n = 256, 700
+    rows = orc.gen_rows(d, 48, 0.97, 0.05, 32.0, 4, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, 1 / 64, 4, 1000)
+    ev_ref = ref.update_block(rows, ts)
+    s = prod.AttpState(d, 1 / 64, seed=4, stream=1000)
+    ev = s.update_block(rows, ts)
+    assert ev_ref["reduced"].sum() >= 3
+    assert_trace_equal(ev, ev_ref, rtol=1e-7)
+    assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-8
+
+
+# ---------------------------------------------------------------- sliding window
+def test_ml_bookkeeping_bit_exact(orc):
+    """acceptance.cpp check 5 shape: MlState queue/level indexing bit-exact."""
+    d, n_win, eps, T = 32, 500, 0.2, 1500
+    ref = orc.MlState(d, n_win, 32.0, eps, 0, 1000)
+    s = prod.MlState(d, n_win, 32.0, eps, seed=0, stream=1000)
+    g = orc.OracleGram(d, n_win)
+    rows = uniform_rows(orc, T, d, 0, 0)
+    # heavy rows: a few rows scaled above the lower thresholds
+    rows[[100, 700, 1200]] *= 25.0
+    for b in range(0, T, 100):
+        blk, ts = rows[b:b + 100], np.arange(b + 1, b + 101)
+        ref.update_block(blk, ts)
+        s.update_block(blk, ts)
+        g.add_block(blk, ts)
+        qi = s.info()
+        ri = ref.info()
+        assert (qi.clock, qi.norm_warnings, qi.levels) == (ri["clock"], ri["norm_warnings"], ri["levels"])
+        assert abs(qi.window_mass - ri["window_mass"]) <= 1e-9 * ri["window_mass"]
+        for j in range(s.levels):
+            mine = [(x[1], x[2], x[0]) for x in s.level_state(j).snap_meta()]
+            theirs = [(x["s"], x["t"], x["z"].shape[1]) for x in ref.level_state(j).snaps()]
+            assert mine == theirs, (j, b)
+            assert [(h["s"], h["t"]) for h in s.heavy(j)] == [(h["s"], h["t"]) for h in ref.heavy(j)]
+        q, qr = s.query(), ref.query()
+        assert (q["level"], q["fallback"], q["xi_sum"], q["heavy_used"]) == \
+            (qr["level"], qr["fallback"], qr["xi_sum"], qr["heavy_used"])
+        e_gpu, e_ref = g.error(q["sketch"]), g.error(qr["sketch"])
+        assert e_gpu <= eps and abs(e_gpu - e_ref) <= 1e-6
+
+
+# ---------------------------------------------------------------- distributed
+def test_distributed_merge_parity(orc):
+    """acceptance.cpp check 9 shape: m sites with per-site thresholds from the
+    norm-only replay, contributions absorbed by the coordinator accumulator,
+    probe = merged Gram; errors and protocol bytes match the oracle simulator."""
+    m, d, eps, T, qe = 4, 32, 0.2, 600, 100
+    streams = np.stack([uniform_rows(orc, T, d, 3, j) for j in range(m)])
+    ref = orc.dist_run(streams, eps, query_every=qe, seed=3)
+    sq = np.cumsum(streams * streams, axis=-1)[..., -1]
+    theta, mass_bytes, bc = prod.dist_theta_schedule(sq, eps)
+    assert bc == ref["broadcasts"]
+    sites = [prod.AeroState(d, eps, 0.0, seed=3, stream=1000 + j) for j in range(m)]
+    coord = prod.Coordinator(d, m)
+    ell = sites[0].ell
+    bytes_total = mass_bytes
+    g = orc.OracleGram(d)
+    errs = []
+    for b in range(0, T, qe):
+        ts = np.arange(b + 1, b + qe + 1)
+        for j in range(m):
+            sites[j].update_block(streams[j, b:b + qe], ts, thetas=theta[j, b:b + qe])
+            bytes_total += coord.absorb(sites[j])
+            g.add_block(streams[j, b:b + qe], ts)
+        sk, _ = coord.probe(sites, ell)
+        errs.append(g.error(sk))
+    assert bytes_total == ref["comm_bytes"]
+    assert np.all(np.array(errs) <= eps)
+    assert np.max(np.abs(np.array(errs) - ref["probe_err"])) <= 1e-6
+
+
+def test_single_site_equals_attp(orc):  # test_distributed.cpp:161-194
+    d, eps, T = 8, 0.25, 300
+    rows = uniform_rows(orc, T, d, 5, 0)
+    theta, _, _ = prod.dist_theta_schedule(np.cumsum(rows * rows, axis=-1)[:, -1][None], eps)
+    site = prod.AeroState(d, eps, 0.0, seed=5, stream=1000)
+    ev_site = site.update_block(rows, np.arange(1, T + 1), thetas=theta[0])
+    attp = prod.AttpState(d, eps, seed=5, stream=1000)
+    ev_attp = attp.update_block(rows, np.arange(1, T + 1))
+    assert_trace_equal(ev_site, ev_attp, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- generator
+def test_device_generator_matches_oracle(orc):
+    n = 64
+    out = torch.empty((n, 1024), dtype=torch.float64, device="cuda")
+    prod.gen_rows_device(out, 5, 1024, 32, 0.9, 0.1, 64.0, seed=1)
+    torch.cuda.synchronize()
+    ref = orc.gen_rows(1024, 32, 0.9, 0.1, 64.0, 1, 0, 5, n)
+    assert np.max(np.abs(out.cpu().numpy() - ref)) < 1e-12 * np.max(np.abs(ref))
+
+
+def test_kernels_launched():
+    n0 = prod.kernel_launches()
+    s = prod.AttpState(64, 0.25, seed=1)
+    s.update_block(np.random.default_rng(1).standard_normal((50, 64)), np.arange(1, 51))
+    assert prod.kernel_launches() > n0
