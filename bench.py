@@ -274,6 +274,10 @@ def main():
             "stats": {"gate_fire_rate": float(ev["gate_fired"].mean()), "dump_rate": float(ev["dumped"].mean()),
                       "reduces": int(ev["reduced"].sum()), "batches": int(info.device_batches),
                       "mispredicts": int(info.device_mispredicts), "snap_cols": int(info.snap_cols),
+                      "batch_end": {"nofire": int(info.end_nofire), "fired": int(info.end_fired),
+                                    "doubling": int(info.end_doubling), "dump": int(info.end_dump)},
+                      "doubling_steps_hist": np.bincount(ev["doubling_steps"]).tolist(),
+                      "xi_hist": np.bincount(ev["xi"]).tolist(),
                       "iterate_ms": prof["iterate_ms"], "reduce_ms": prof["reduce_ms"],
                       "product_ms": prof["product_ms"], "product_launches": int(prof["product_launches"])},
         }

@@ -71,6 +71,9 @@ typedef struct aero_info {
     int64_t snap_cols;          /* sum of snapshot widths (xi) in the queue */
     double theta, fro_mass;     /* fro_mass: AttpState::fro_mass (attp.hpp:34) */
     int64_t device_rows_processed, device_batches, device_mispredicts;
+    /* batch-ending causes: predicted fire but the gate did not; predicted no
+     * fire but it did; a larger doubling rank was needed; a dump */
+    int64_t end_nofire, end_fired, end_doubling, end_dump;
 } aero_info;
 
 /* ---- AeroState / AttpState --------------------------------------------- */
@@ -209,6 +212,11 @@ const char* aero_last_error(void);  /* thread-local text of the last failure */
 const char* aero_version(void);
 /* device kernels launched by this library so far (all handles, this process) */
 int64_t aero_kernel_launches(void);
+/* symmetric eigensolver used by the FD reduce and the query shrink (test
+ * hook; linalg.cpp:60-77 semantics): a is n x n row-major (symmetrized),
+ * w descending, v columns = eigenvectors sign-fixed; device_ms (nullable)
+ * receives the device time of the solve */
+int aero_eigh(int32_t n, const double* a, double* w, double* v, double* device_ms);
 /* RngState draws on the device (test hook): count gaussians of fork #fork of
  * RngState(seed, stream) (fork 0 = the root), to host memory */
 int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out);

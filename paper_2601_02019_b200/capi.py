@@ -76,7 +76,8 @@ class Info(C.Structure):
     _fields_ = [("d", i32), ("ell", i32), ("rows", i32), ("clock", i64), ("last_dump_t", i64),
                 ("forks", i64), ("snaps", i64), ("snap_cols", i64), ("theta", f64),
                 ("fro_mass", f64), ("device_rows_processed", i64), ("device_batches", i64),
-                ("device_mispredicts", i64)]
+                ("device_mispredicts", i64), ("end_nofire", i64), ("end_fired", i64),
+                ("end_doubling", i64), ("end_dump", i64)]
 
 
 class Profile(C.Structure):
@@ -151,6 +152,7 @@ SIGNATURES = [
     ("aero_version", C.c_char_p, []),
     ("aero_kernel_launches", i64, []),
     ("aero_rng_gaussians", i32, [u64, u64, i64, i64, P(f64)]),
+    ("aero_eigh", i32, [i32, P(f64), P(f64), P(f64), P(f64)]),
 ]
 
 _lib = None
@@ -196,6 +198,15 @@ def rng_gaussians(seed, stream, fork, count):
     out = np.empty(count)
     _chk(lib().aero_rng_gaussians(seed, stream, fork, count, _dp(out)))
     return out
+
+
+def eigh(b, return_ms=False):
+    """Device symmetric eigensolver (linalg.cpp:60-77 semantics)."""
+    b = _f64(b)
+    n = b.shape[0]
+    w, v, ms = np.empty(n), np.empty((n, n)), f64()
+    _chk(lib().aero_eigh(n, _dp(b), _dp(w), _dp(v), C.byref(ms)))
+    return (w, v, ms.value) if return_ms else (w, v)
 
 
 def _device_ptr(x):

@@ -180,6 +180,39 @@ int aero_reset_profile(aero_sketch* h) {
     return AERO_OK;
 }
 
+int aero_eigh(int32_t n, const double* a, double* w, double* v, double* device_ms) {
+    REQ(a);
+    REQ(w);
+    REQ(v);
+    return guard([&] {
+        if (n < 1) throw InvalidInput("eigh: empty input");
+        double *dA = nullptr, *dw = nullptr;
+        AERO_CUDA(cudaMalloc(&dA, sizeof(double) * (size_t)n * n));
+        AERO_CUDA(cudaMalloc(&dw, sizeof(double) * n));
+        // row-major symmetric input == its column-major transpose
+        AERO_CUDA(cudaMemcpy(dA, a, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, 0);
+        eigh(0, n, dA, n, dw);
+        cudaEventRecord(e1, 0);
+        AERO_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (device_ms) *device_ms = ms;
+        std::vector<double> cm((size_t)n * n);
+        AERO_CUDA(cudaMemcpy(cm.data(), dA, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost));
+        AERO_CUDA(cudaMemcpy(w, dw, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) v[(size_t)i * n + j] = cm[i + (size_t)j * n];
+        cudaFree(dA);
+        cudaFree(dw);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
 int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out) {
     REQ(out);
     return guard([&] {

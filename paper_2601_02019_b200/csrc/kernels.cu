@@ -184,9 +184,10 @@ void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int
 // On return diag(A) holds the eigenvalues (unsorted) and V the eigenvectors.
 // ============================================================================
 struct JacobiScratch {
-    double* cs;   // 2 * (n/2+1)
-    int* flag;    // 1
+    double* cs;  // >= jacobi_scratch_doubles(n) doubles
 };
+__device__ int g_jacobi_sweeps = 0;  // diagnostics: max sweeps used (1000 = cap hit)
+__host__ __device__ constexpr int jacobi_scratch_doubles(int n) { return 6 * (n / 2 + 3); }
 __device__ void cta_jacobi(double* A, double* V, int n, JacobiScratch sc) {
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < n * n; e += nt) V[e] = (e % (n + 1) == 0) ? 1.0 : 0.0;
@@ -194,46 +195,69 @@ __device__ void cta_jacobi(double* A, double* V, int n, JacobiScratch sc) {
     if (n <= 1) return;
     const int np = n + (n & 1);  // players (dummy = n when odd)
     const int half = np / 2;
-    for (int sweep = 0; sweep < 60; ++sweep) {
-        if (tid == 0) *sc.flag = 0;
+    double* crs = sc.cs;                                   // c, s, t per pair
+    double* tolp = crs + 3 * half;                         // 1 double
+    int* pidx = reinterpret_cast<int*>(tolp + 2);          // p, q per pair
+    int* flag = pidx + 2 * half + 2;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) {
+            // absolute floor: rotations below ~eps*||A|| are rounding noise
+            double sc_max = 0.0;
+            for (int i = 0; i < n; ++i) sc_max = fmax(sc_max, fabs(A[i + i * n]));
+            *tolp = 1.0e-16 * sc_max;
+            *flag = 0;
+        }
         __syncthreads();
+        const double tol_abs = *tolp;
         for (int step = 0; step < np - 1; ++step) {
-            // (a) rotation parameters for the disjoint pairs of this step
+            // (a) disjoint pairs of this round-robin step and their rotations
             for (int i = tid; i < half; i += nt) {
                 const int pi = (i == 0) ? 0 : ((i - 1 + step) % (np - 1)) + 1;
                 const int qi = ((np - 1 - i - 1 + step) % (np - 1)) + 1;
-                int p = min(pi, qi), q = max(pi, qi);
-                double c = 1.0, s = 0.0;
+                const int p = min(pi, qi), q = max(pi, qi);
+                double c = 1.0, s = 0.0, t = 0.0;
                 if (q < n) {
                     const double apq = A[p + q * n];
                     const double app = A[p + p * n], aqq = A[q + q * n];
-                    if (fabs(apq) > 1e-300 &&
-                        fabs(apq) > 1.1102230246251565e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+                    if (fabs(apq) > 1e-300 && fabs(apq) > tol_abs &&
+                        fabs(apq) > 2.220446049250313e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
                         const double tau = (aqq - app) / (2.0 * apq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                         c = 1.0 / sqrt(1.0 + t * t);
                         s = t * c;
-                        *sc.flag = 1;
+                        *flag = 1;
                     }
                 }
-                sc.cs[2 * i] = c;
-                sc.cs[2 * i + 1] = s;
+                crs[3 * i] = c;
+                crs[3 * i + 1] = s;
+                crs[3 * i + 2] = t;
+                pidx[2 * i] = p;
+                pidx[2 * i + 1] = q;
             }
             __syncthreads();
-            // (b) A <- R^T A R on 2x2 blocks of pair pairs; V <- V R
+            // (b) A <- R^T A R on the 2x2 blocks of pair pairs (diagonal blocks
+            // updated exactly, GVL Alg. 8.4.2); V <- V R
             const int nblk = half * half;
             for (int bidx = tid; bidx < nblk + half * n; bidx += nt) {
                 if (bidx < nblk) {
                     const int I = bidx % half, J = bidx / half;
-                    const int pI0 = (I == 0) ? 0 : ((I - 1 + step) % (np - 1)) + 1;
-                    const int qI0 = ((np - 1 - I - 1 + step) % (np - 1)) + 1;
-                    const int pJ0 = (J == 0) ? 0 : ((J - 1 + step) % (np - 1)) + 1;
-                    const int qJ0 = ((np - 1 - J - 1 + step) % (np - 1)) + 1;
-                    const int p = min(pI0, qI0), q = max(pI0, qI0);
-                    const int pp = min(pJ0, qJ0), qq = max(pJ0, qJ0);
-                    const double cI = sc.cs[2 * I], sI = sc.cs[2 * I + 1];
-                    const double cJ = sc.cs[2 * J], sJ = sc.cs[2 * J + 1];
+                    const int p = pidx[2 * I], q = pidx[2 * I + 1];
+                    const int pp = pidx[2 * J], qq = pidx[2 * J + 1];
+                    const double cI = crs[3 * I], sI = crs[3 * I + 1];
+                    const double cJ = crs[3 * J], sJ = crs[3 * J + 1];
                     const bool qin = q < n, qqin = qq < n;
+                    if (I == J) {
+                        if (sI != 0.0) {
+                            const double tI = crs[3 * I + 2];
+                            const double apq = A[p + q * n];
+                            A[p + p * n] -= tI * apq;
+                            A[q + q * n] += tI * apq;
+                            A[p + q * n] = 0.0;
+                            A[q + p * n] = 0.0;
+                        }
+                        continue;
+                    }
+                    if (sI == 0.0 && sJ == 0.0) continue;
                     const double b00 = A[p + pp * n];
                     const double b01 = qqin ? A[p + qq * n] : 0.0;
                     const double b10 = qin ? A[q + pp * n] : 0.0;
@@ -247,13 +271,13 @@ __device__ void cta_jacobi(double* A, double* V, int n, JacobiScratch sc) {
                     if (qin) A[q + pp * n] = cJ * l10 - sJ * l11;
                     if (qin && qqin) A[q + qq * n] = sJ * l10 + cJ * l11;
                 } else {
+                    // consecutive threads walk consecutive rows (conflict-free)
                     const int e = bidx - nblk;
-                    const int I = e % half, row = e / half;
-                    const int pI0 = (I == 0) ? 0 : ((I - 1 + step) % (np - 1)) + 1;
-                    const int qI0 = ((np - 1 - I - 1 + step) % (np - 1)) + 1;
-                    const int p = min(pI0, qI0), q = max(pI0, qI0);
-                    if (q >= n) continue;
-                    const double c = sc.cs[2 * I], s = sc.cs[2 * I + 1];
+                    const int row = e % n, I = e / n;
+                    const int p = pidx[2 * I], q = pidx[2 * I + 1];
+                    const double s = crs[3 * I + 1];
+                    if (q >= n || s == 0.0) continue;
+                    const double c = crs[3 * I];
                     const double vp = V[row + p * n], vq = V[row + q * n];
                     V[row + p * n] = c * vp - s * vq;
                     V[row + q * n] = s * vp + c * vq;
@@ -261,8 +285,12 @@ __device__ void cta_jacobi(double* A, double* V, int n, JacobiScratch sc) {
             }
             __syncthreads();
         }
-        if (*sc.flag == 0) break;
+        if (*flag == 0) {
+            if (tid == 0) atomicMax(&g_jacobi_sweeps, sweep + 1);
+            break;
+        }
         __syncthreads();
+        if (sweep == 39 && tid == 0) atomicMax(&g_jacobi_sweeps, 1000);
     }
     __syncthreads();
 }
@@ -298,7 +326,6 @@ __global__ void k_jacobi_batched(int n, double* A, int lda, int64_t stride, doub
     double* sA = sm;
     double* sV = sA + n * n;
     double* cs = sV + n * n;
-    int* flag = reinterpret_cast<int*>(cs + 2 * (n / 2 + 2));
     double* Ab = A + blockIdx.x * stride;
     double* wb = w + blockIdx.x * (int64_t)n;
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
@@ -306,16 +333,16 @@ __global__ void k_jacobi_batched(int n, double* A, int lda, int64_t stride, doub
         sA[e] = 0.5 * (Ab[i + (int64_t)j * lda] + Ab[j + (int64_t)i * lda]);
     }
     __syncthreads();
-    cta_jacobi(sA, sV, n, JacobiScratch{cs, flag});
+    cta_jacobi(sA, sV, n, JacobiScratch{cs});
     cta_sort_signfix(sA, sV, n, wb, Ab, lda);
 }
 
 void eigh_small(cudaStream_t st, int n, double* A, int lda, double* w, int batch, int64_t stride) {
-    const size_t smem = sizeof(double) * (2 * n * n + 2 * (n / 2 + 2)) + 16;
+    const size_t smem = sizeof(double) * (2 * n * n + jacobi_scratch_doubles(n)) + 16;
     if (smem > 48 * 1024)
         AERO_CUDA(cudaFuncSetAttribute(k_jacobi_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    k_jacobi_batched<<<batch, 256, smem, st>>>(n, A, lda, stride, w);
+    k_jacobi_batched<<<batch, n >= 48 ? 512 : 256, smem, st>>>(n, A, lda, stride, w);
     AERO_LAUNCHED();
 }
 
@@ -417,8 +444,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     double* W = S + max_k * max_k;          // k*k
     double* T = W + max_k * max_k;          // k*k
     double* lam = T + max_k * max_k;        // k
-    double* cs = lam + max_k;               // 2*(k/2+2)
-    int* flag = reinterpret_cast<int*>(cs + 2 * (max_k / 2 + 2));
+    double* cs = lam + max_k;               // jacobi scratch
     if (st != JOB_ACTIVE) {
         if (last && tid == 0) {
             if (jb.type == 0) out_sig[jb.col] = 0.0;
@@ -453,7 +479,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
     }
     __syncthreads();
-    cta_jacobi(W, T, k, JacobiScratch{cs, flag});  // W -> diag, T -> eigvecs
+    cta_jacobi(W, T, k, JacobiScratch{cs});  // W -> diag, T -> eigvecs
     // lam_i and T columns scaled by lam^{-1/2} with clamp
     if (tid == 0) {
         double lmax = 0.0;
@@ -496,7 +522,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
     }
     __syncthreads();
-    cta_jacobi(W, T, k, JacobiScratch{cs, flag});
+    cta_jacobi(W, T, k, JacobiScratch{cs});
     double* vr = out_vr + (int64_t)jb.col * kv;
     cta_sort_signfix(W, T, k, lam, vr, k);
     for (int a = tid; a < k; a += nt) out_sig[jb.col + a] = sqrt(fmax(lam[a], 0.0));
@@ -507,7 +533,7 @@ void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, 
                     double* out_vr, int kv, int* out_clamped, int max_k) {
     if (njobs <= 0) return;
     const size_t smem =
-        sizeof(double) * (32 * 16 + 3 * max_k * max_k + max_k + 2 * (max_k / 2 + 2)) + 16;
+        sizeof(double) * (32 * 16 + 3 * max_k * max_k + max_k + jacobi_scratch_doubles(max_k)) + 16;
     if (smem > 48 * 1024)
         AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));

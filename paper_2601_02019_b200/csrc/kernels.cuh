@@ -16,6 +16,12 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha,
            int lda, const double* B, int ldb, double beta, double* D, int ldd,
            const int* colmask = nullptr);
 
+// the dominant product Y = A B (A: M x K, B: K x N, column-major) with the
+// per-column row mask; split-K partials go through ws (product.cu)
+size_t product_workspace_doubles(int M, int N);
+void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
+                  int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles);
+
 // per-row squared norm and finiteness of n rows (row-major, ld) -> nrm2[n], bad[n]
 void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int d, double* nrm2,
                  int* bad);

@@ -102,6 +102,7 @@ Sketch::Sketch(const aero_cfg& cfg) {
     X_.alloc((size_t)ldx_ * ncols_);
     Y_.alloc((size_t)ldx_ * ncols_);
     H_.alloc((size_t)ldx_ * ncols_);
+    ws_.alloc(product_workspace_doubles(cap_, ncols_));
     sig_.alloc(ncols_);
     vr_.alloc((size_t)ncols_ * kv_);
     small_.alloc(4 * 64 * 64 + 64);
@@ -258,8 +259,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
                 flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
             }
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2 + 2 * p), st_));
-        dgemm(st_, false, false, R, ncol, R, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_,
-              colmask_d_);
+        gemm_product(st_, R, ncol, R, G_.p, cap_, X_.p, ldx_, Y_.p, ldx_, colmask_d_, ws_.p, ws_.n);
         if (profiling) {
             AERO_CUDA(cudaEventRecord(ev_at(3 + 2 * p), st_));
             prof.product_launches++;
@@ -308,7 +308,7 @@ void Sketch::run_simul_large(int k, uint64_t rng0, int r) {
         return;
     }
     for (int p = 0; p <= q_; ++p) {
-        dgemm(st_, false, false, r, k, r, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_, colmask_d_);
+        gemm_product(st_, r, k, r, G_.p, cap_, X_.p, ldx_, Y_.p, ldx_, colmask_d_, ws_.p, ws_.n);
         dgemm(st_, true, false, k, k, r, 1.0, X_.p, ldx_, Y_.p, ldx_, 0.0, S, k);
         eigh(st_, k, S, k, lam);
         k_inv_sqrt_clamp<<<1, 1, 0, st_>>>(lam, k, sc);
@@ -435,7 +435,9 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
                           const double* thetas, aero_event* log) {
     const int r0 = r_;
     const uint64_t F = forks_;
-    const Pattern pat = pattern_;
+    // predict the majority outcome of recent rows (a lone non-firing row in a
+    // firing regime ends one batch, not two)
+    const Pattern pat = (fire_ema_ >= 0.5) ? FIRE1 : NOFIRE;
     append_rows(dev_rows, B);
     const int R = r0 + (int)B;
     int njobs = 0;
@@ -472,6 +474,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
         const bool fire = s1 >= 0.5 * theta;
         const int rj = r0 + (int)j + 1;
         auto commit = [&]() {
+            fire_ema_ = 0.95 * fire_ema_ + 0.05 * (ev->gate_fired ? 1.0 : 0.0);
             r_ = rj;
             clock_ = t[j];
             ev->forks_after = (int64_t)forks_;
@@ -489,6 +492,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
                 commit();
                 pattern_ = FIRE1;
                 mispredicts++;
+                end_fired++;
                 return j + 1;
             }
             commit();
@@ -501,6 +505,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
             commit();
             pattern_ = NOFIRE;
             mispredicts++;
+            end_nofire++;
             return j + 1;
         }
         ev->gate_fired = 1;
@@ -529,7 +534,10 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
                 ev->dumped = 1;
                 commit();
                 pattern_ = FIRE1;
-                if (j + 1 < B) mispredicts++;
+                if (j + 1 < B) {
+                    mispredicts++;
+                    end_dump++;
+                }
                 return j + 1;
             }
             commit();
@@ -541,6 +549,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
         commit();
         pattern_ = FIRE1;
         mispredicts++;
+        end_doubling++;
         return j + 1;
     }
     pattern_ = pat;
@@ -559,6 +568,7 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
             ev->theta = thetas[pos];
             theta_ = thetas[pos];
             single_row(dev_rows + (size_t)pos * d_, t[pos], thetas[pos], ev);
+            fire_ema_ = 0.95 * fire_ema_ + 0.05 * (ev->gate_fired ? 1.0 : 0.0);
             rows_processed++;
             pos++;
             continue;
@@ -770,6 +780,10 @@ void Sketch::info(aero_info* o) const {
     o->device_rows_processed = rows_processed;
     o->device_batches = batches;
     o->device_mispredicts = mispredicts;
+    o->end_nofire = end_nofire;
+    o->end_fired = end_fired;
+    o->end_doubling = end_doubling;
+    o->end_dump = end_dump;
 }
 
 }  // namespace aero_b200

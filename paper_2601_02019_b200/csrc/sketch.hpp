@@ -79,6 +79,7 @@ class Sketch {
 
     // counters
     int64_t rows_processed = 0, batches = 0, mispredicts = 0;
+    int64_t end_nofire = 0, end_fired = 0, end_doubling = 0, end_dump = 0;
     aero_profile prof{};
     bool profiling = false;
 
@@ -119,12 +120,13 @@ class Sketch {
     uint64_t forks_ = 0;
     int r_ = 0;
     Pattern pattern_ = FIRE1;
+    double fire_ema_ = 1.0;  // moving average of gate fires (batch prediction)
     std::deque<SnapRec> snaps_;
     std::deque<Chunk*> chunks_;
     aero_event last_ev_{};
     // device buffers
     DeviceBuf C_, C2_, G_, E_, ew_, fw_, stage_, nrm_, X_, Y_, H_, sig_, vr_, small_, Bq_, Wq_,
-        qw_, qy_;
+        qw_, qy_, ws_;
     int* status_d_ = nullptr;
     int* clamp_d_ = nullptr;
     int* colmask_d_ = nullptr;
