@@ -384,32 +384,39 @@ void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G,
 }
 
 // k x k Gram of two column blocks P (r x k) and Q (r x k), ld, into S (smem, col-major)
+template <int KM>
 __device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k, double* S,
                          double* red) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int E = k * k;
-    if (E <= 16) {
-        double part[16];
+    if (KM <= 4) {
+        // register partials (k <= KM <= 4, compile-time indexed), warp + CTA sums
+        double part[KM * KM];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) part[e] = 0.0;
+        for (int e = 0; e < KM * KM; ++e) part[e] = 0.0;
         for (int i = tid; i < r; i += nt) {
-            double p[4], q[4];
-            for (int a = 0; a < k; ++a) {
-                p[a] = P[i + (int64_t)a * ld];
-                q[a] = Q[i + (int64_t)a * ld];
+            double p[KM], q[KM];
+#pragma unroll
+            for (int a = 0; a < KM; ++a) {
+                p[a] = (a < k) ? P[i + (int64_t)a * ld] : 0.0;
+                q[a] = (a < k) ? Q[i + (int64_t)a * ld] : 0.0;
             }
-            for (int a = 0; a < k; ++a)
-                for (int b = 0; b < k; ++b) part[a + b * k] = fma(p[a], q[b], part[a + b * k]);
+#pragma unroll
+            for (int a = 0; a < KM; ++a)
+#pragma unroll
+                for (int b = 0; b < KM; ++b) part[a + b * KM] = fma(p[a], q[b], part[a + b * KM]);
         }
         const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
-        for (int e = 0; e < E; ++e) {
+#pragma unroll
+        for (int e = 0; e < KM * KM; ++e) {
             const double v = warp_sum(part[e]);
             if (lane == 0) red[wid * 16 + e] = v;
         }
         __syncthreads();
         for (int e = tid; e < E; e += nt) {
+            const int a = e % k, b = e / k;
             double t = 0.0;
-            for (int w = 0; w < nw; ++w) t += red[w * 16 + e];
+            for (int w = 0; w < nw; ++w) t += red[w * 16 + a + b * KM];
             S[e] = t;
         }
         __syncthreads();
@@ -425,11 +432,42 @@ __device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k,
     }
 }
 
+// eigendecomposition of a k x k symmetric W (shared memory) -> diag(W), T:
+// closed-form 2x2 Jacobi rotation (GVL Alg. 8.4.1) for k <= 2, CTA Jacobi else
+__device__ void small_eig(double* W, double* T, int k, double* cs) {
+    if (k > 2) {
+        cta_jacobi(W, T, k, JacobiScratch{cs});
+        return;
+    }
+    if (threadIdx.x == 0) {
+        if (k == 1) {
+            T[0] = 1.0;
+        } else {
+            const double a = W[0], b = W[2], c = W[3];
+            double cn = 1.0, sn = 0.0, t = 0.0;
+            if (fabs(b) > 1e-300) {
+                const double tau = (c - a) / (2.0 * b);
+                t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                cn = 1.0 / sqrt(1.0 + t * t);
+                sn = t * cn;
+            }
+            W[0] = a - t * b;
+            W[3] = c + t * b;
+            W[1] = W[2] = 0.0;
+            T[0] = cn;
+            T[1] = -sn;
+            T[2] = sn;
+            T[3] = cn;
+        }
+    }
+    __syncthreads();
+}
+
+template <int KM>
 __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, double* X,
                                  const double* __restrict__ Y, int ldx, double* H,
                                  int* __restrict__ status, double* __restrict__ out_sig,
-                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
-                                 int max_k) {
+                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped) {
     extern __shared__ double sm[];
     const IterJob jb = jobs[blockIdx.x];
     if (phase >= jb.nphase) return;
@@ -439,12 +477,12 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     const int r = jb.r, k = jb.k;
     double* x = X + (int64_t)jb.col * ldx;
     const double* y = Y + (int64_t)jb.col * ldx;
-    double* red = sm;                       // 32*16
-    double* S = red + 32 * 16;              // k*k
-    double* W = S + max_k * max_k;          // k*k
-    double* T = W + max_k * max_k;          // k*k
-    double* lam = T + max_k * max_k;        // k
-    double* cs = lam + max_k;               // jacobi scratch
+    double* red = sm;                  // 32*16
+    double* S = red + 32 * 16;         // KM*KM
+    double* W = S + KM * KM;           // KM*KM
+    double* T = W + KM * KM;           // KM*KM
+    double* lam = T + KM * KM;         // KM
+    double* cs = lam + KM;             // jacobi scratch
     if (st != JOB_ACTIVE) {
         if (last && tid == 0) {
             if (jb.type == 0) out_sig[jb.col] = 0.0;
@@ -473,13 +511,13 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
         return;
     }
     // simul: S = X^T Y (Gram of g = C'^T X), T = S^{-1/2}
-    cta_gram(x, y, ldx, r, k, S, red);
+    cta_gram<KM>(x, y, ldx, r, k, S, red);
     for (int e = tid; e < k * k; e += nt) {
         const int a = e % k, b = e / k;
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
     }
     __syncthreads();
-    cta_jacobi(W, T, k, JacobiScratch{cs});  // W -> diag, T -> eigvecs
+    small_eig(W, T, k, cs);  // W -> diag, T -> eigvecs
     // lam_i and T columns scaled by lam^{-1/2} with clamp
     if (tid == 0) {
         double lmax = 0.0;
@@ -498,16 +536,24 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     __syncthreads();
     // rows independent: [last: H = X T], X <- Y T
     for (int i = tid; i < r; i += nt) {
-        double xr[64], yr[64];
-        for (int a = 0; a < k; ++a) {
-            xr[a] = x[i + (int64_t)a * ldx];
-            yr[a] = y[i + (int64_t)a * ldx];
+        double xr[KM], yr[KM];
+#pragma unroll
+        for (int a = 0; a < KM; ++a) {
+            if (a < k) {
+                xr[a] = x[i + (int64_t)a * ldx];
+                yr[a] = y[i + (int64_t)a * ldx];
+            }
         }
-        for (int b = 0; b < k; ++b) {
+#pragma unroll
+        for (int b = 0; b < KM; ++b) {
+            if (b >= k) break;
             double hx = 0.0, hy = 0.0;
-            for (int a = 0; a < k; ++a) {
-                hx = fma(xr[a], T[a + b * k], hx);
-                hy = fma(yr[a], T[a + b * k], hy);
+#pragma unroll
+            for (int a = 0; a < KM; ++a) {
+                if (a < k) {
+                    hx = fma(xr[a], T[a + b * k], hx);
+                    hy = fma(yr[a], T[a + b * k], hy);
+                }
             }
             if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;
             x[i + (int64_t)b * ldx] = hy;
@@ -516,30 +562,42 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     __syncthreads();
     if (!last) return;
     // Ritz values: eig(w^T w), w = C' g = G H = X (linalg.cpp:145-150)
-    cta_gram(x, x, ldx, r, k, S, red);
+    cta_gram<KM>(x, x, ldx, r, k, S, red);
     for (int e = tid; e < k * k; e += nt) {
         const int a = e % k, b = e / k;
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
     }
     __syncthreads();
-    cta_jacobi(W, T, k, JacobiScratch{cs});
+    small_eig(W, T, k, cs);
     double* vr = out_vr + (int64_t)jb.col * kv;
     cta_sort_signfix(W, T, k, lam, vr, k);
     for (int a = tid; a < k; a += nt) out_sig[jb.col + a] = sqrt(fmax(lam[a], 0.0));
+}
+
+template <int KM>
+static void launch_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
+                             const double* Y, int ldx, double* H, int* status, double* out_sig,
+                             double* out_vr, int kv, int* out_clamped) {
+    const size_t smem =
+        sizeof(double) * (32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM)) + 16;
+    if (smem > 48 * 1024)
+        AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    k_iter_normalize<KM><<<njobs, 256, smem, st>>>(jobs, phase, X, Y, ldx, H, status, out_sig, out_vr,
+                                                   kv, out_clamped);
+    AERO_LAUNCHED();
 }
 
 void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
                     const double* Y, int ldx, double* H, int* status, double* out_sig,
                     double* out_vr, int kv, int* out_clamped, int max_k) {
     if (njobs <= 0) return;
-    const size_t smem =
-        sizeof(double) * (32 * 16 + 3 * max_k * max_k + max_k + jacobi_scratch_doubles(max_k)) + 16;
-    if (smem > 48 * 1024)
-        AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    k_iter_normalize<<<njobs, 256, smem, st>>>(jobs, phase, X, Y, ldx, H, status, out_sig, out_vr,
-                                               kv, out_clamped, max_k);
-    AERO_LAUNCHED();
+    if (max_k <= 2)
+        launch_normalize<2>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+    else if (max_k <= 4)
+        launch_normalize<4>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+    else
+        launch_normalize<64>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
 }
 
 // ============================================================================

@@ -19,6 +19,11 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha,
 // the dominant product Y = A B (A: M x K, B: K x N, column-major) with the
 // per-column row mask; split-K partials go through ws (product.cu)
 size_t product_workspace_doubles(int M, int N);
+// Y = op(A) op(B) on the fast path (alpha = 1, beta = 0); returns false (and
+// does nothing) when operand alignment rules it out -- callers then use dgemm
+bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+              const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
+              size_t ws_doubles);
 void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
                   int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles);
 

@@ -1,11 +1,15 @@
-// The dominant kernel of the update path: the batched power / subspace
-// iteration product Y = G X (G: R x R Gram of the row buffer, X: R x N job
-// columns; reference linalg.cpp:109-118 and :141-143 in Gram form).
+// The large fp64 contractions of the update path, led by the dominant one:
+// the batched power / subspace iteration product Y = G X (G: R x R Gram of the
+// row buffer, X: R x N job columns; reference linalg.cpp:109-118 and :141-143
+// in Gram form), plus the buffer-append Gram block (C'^T C'_new, K = d) and
+// the FD-reduce rotation / re-Gram.
 // fp64 DFMA, 128x64 CTA tile, 8x8 register micro-tile per thread (DFMA-bound,
-// shared memory at ~50%), cp.async double-buffered 16-deep K slices, and a
-// deterministic split-K (fixed-order reduction) so that R ~ 2048, N ~ 192
-// fills all 148 SMs. Column-major throughout; rows >= colmask[j] of output
-// column j are written as 0 (each job's prefix length).
+// shared memory at ~50%), 3-stage cp.async pipeline over 16-deep K slices, and
+// a deterministic split-K (fixed-order reduction) so skinny shapes fill all
+// 148 SMs with two CTAs each. Column-major; op(A) = A or A^T, op(B) = B or B^T.
+// Rows >= colmask[j] of output column j are written as 0 (job prefix lengths).
+#include <algorithm>
+
 #include "aero_common.cuh"
 #include "kernels.cuh"
 
@@ -13,11 +17,10 @@ namespace aero_b200 {
 
 namespace {
 constexpr int PBM = 128, PBN = 64, PBK = 16, PNT = 128, PST = 3;  // PST cp.async stages
-constexpr int BLD = PBK + 2;  // padded k-stride of the B tile (conflict-free)
-struct ProdSmem {
-    double a[PST][PBK][PBM];
-    double b[PST][PBN][BLD];
-};
+constexpr int KLD = PBK + 2;  // padded k-stride for k-contiguous tiles (16B aligned rows)
+constexpr int A_TILE = (PBM * KLD > PBK * PBM) ? PBM * KLD : PBK * PBM;
+constexpr int B_TILE = (PBN * KLD > PBK * PBN) ? PBN * KLD : PBK * PBN;
+constexpr size_t PROD_SMEM = sizeof(double) * (size_t)PST * (A_TILE + B_TILE);
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -30,12 +33,16 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// A tile: !TA -> a[k][m] (m contiguous); TA -> a[m][k] (k contiguous, ld KLD)
+// B tile: !TB -> b[n][k] (k contiguous, ld KLD); TB -> b[k][n] (n contiguous)
+template <bool TA, bool TB>
 __global__ void __launch_bounds__(PNT, 2)
     k_product(int M, int N, int K, int kchunk, const double* __restrict__ A, int lda,
               const double* __restrict__ B, int ldb, double* __restrict__ out, int ldo,
               int64_t split_stride, const int* __restrict__ colmask, int direct) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    ProdSmem& s = *reinterpret_cast<ProdSmem*>(smraw);
+    extern __shared__ __align__(16) double smd[];
+    double* sa = smd;
+    double* sb = smd + PST * A_TILE;
     const int tid = threadIdx.x, tr = tid % 16, tc = tid / 16;
     const int bm = blockIdx.y * PBM, bn = blockIdx.x * PBN;
     const int k0 = blockIdx.z * kchunk, k1 = min(K, k0 + kchunk);
@@ -43,31 +50,49 @@ __global__ void __launch_bounds__(PNT, 2)
 
     auto load_tile = [&](int stage, int kt) {
         const int kb = k0 + kt * PBK;
+        double* ta = sa + stage * A_TILE;
+        double* tb = sb + stage * B_TILE;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {  // A: 16 k-columns x 64 double2
+        for (int i = 0; i < 8; ++i) {  // A: 1024 16-byte chunks
             const int idx = tid + i * PNT;
-            const int col = idx >> 6, r2 = idx & 63;
-            const int gk = kb + col, gm = bm + 2 * r2;
-            int bytes = 0;
-            const double* src = A;
-            if (gk < k1 && gm < M) {
-                bytes = (M - gm >= 2) ? 16 : 8;
-                src = A + gm + (int64_t)gk * lda;
+            int gm, gk, bytes = 0;
+            double* dst;
+            if (!TA) {  // column gk of A: 128 contiguous m
+                const int col = idx >> 6, r2 = idx & 63;
+                gk = kb + col;
+                gm = bm + 2 * r2;
+                dst = ta + col * PBM + 2 * r2;
+                if (gk < k1 && gm < M) bytes = (M - gm >= 2) ? 16 : 8;
+            } else {  // row gm of op(A): 16 contiguous k
+                const int row = idx >> 3, k2 = idx & 7;
+                gm = bm + row;
+                gk = kb + 2 * k2;
+                dst = ta + row * KLD + 2 * k2;
+                if (gm < M && gk < k1) bytes = (k1 - gk >= 2) ? 16 : 8;
             }
-            cp_async16(&s.a[stage][col][2 * r2], src, bytes);
+            const double* src = bytes ? (TA ? A + gk + (int64_t)gm * lda : A + gm + (int64_t)gk * lda) : A;
+            cp_async16(dst, src, bytes);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {  // B: 64 n-columns x 8 double2 (k)
+        for (int i = 0; i < 4; ++i) {  // B: 512 16-byte chunks
             const int idx = tid + i * PNT;
-            const int col = idx >> 3, k2 = idx & 7;
-            const int gn = bn + col, gk = kb + 2 * k2;
-            int bytes = 0;
-            const double* src = B;
-            if (gn < N && gk < k1) {
-                bytes = (k1 - gk >= 2) ? 16 : 8;
-                src = B + gk + (int64_t)gn * ldb;
+            int gn, gk, bytes = 0;
+            double* dst;
+            if (!TB) {  // column gn of B: 16 contiguous k
+                const int col = idx >> 3, k2 = idx & 7;
+                gn = bn + col;
+                gk = kb + 2 * k2;
+                dst = tb + col * KLD + 2 * k2;
+                if (gn < N && gk < k1) bytes = (k1 - gk >= 2) ? 16 : 8;
+            } else {  // row gk of op(B): 64 contiguous n
+                const int row = idx >> 5, n2 = idx & 31;
+                gk = kb + row;
+                gn = bn + 2 * n2;
+                dst = tb + row * PBN + 2 * n2;
+                if (gk < k1 && gn < N) bytes = (N - gn >= 2) ? 16 : 8;
             }
-            cp_async16(&s.b[stage][col][2 * k2], src, bytes);
+            const double* src = bytes ? (TB ? B + gn + (int64_t)gk * ldb : B + gk + (int64_t)gn * ldb) : B;
+            cp_async16(dst, src, bytes);
         }
     };
 
@@ -88,13 +113,17 @@ __global__ void __launch_bounds__(PNT, 2)
         __syncthreads();     // and every warp is done with the stage reloaded below
         if (kt + PST - 1 < nk) load_tile((kt + PST - 1) % PST, kt + PST - 1);
         cp_commit();
+        const double* ta = sa + st * A_TILE;
+        const double* tb = sb + st * B_TILE;
 #pragma unroll
         for (int kk = 0; kk < PBK; ++kk) {
             double av[8], bv[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) av[i] = s.a[st][kk][tr + 16 * i];
+            for (int i = 0; i < 8; ++i)
+                av[i] = TA ? ta[(tr + 16 * i) * KLD + kk] : ta[kk * PBM + tr + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) bv[j] = s.b[st][tc + 8 * j][kk];
+            for (int j = 0; j < 8; ++j)
+                bv[j] = TB ? tb[kk * PBN + tc + 8 * j] : tb[(tc + 8 * j) * KLD + kk];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -130,41 +159,59 @@ __global__ void k_product_reduce(int M, int N, int splits, const double* __restr
     if (colmask && i >= colmask[j]) v = 0.0;
     Y[i + (int64_t)j * ldy] = v;
 }
+
+template <bool TA, bool TB>
+void launch(cudaStream_t st, dim3 grid, int M, int N, int K, int kchunk, const double* A, int lda,
+            const double* B, int ldb, double* out, int ldo, int64_t sstride, const int* colmask,
+            int direct) {
+    static bool attr = false;
+    if (!attr) {
+        AERO_CUDA(cudaFuncSetAttribute(k_product<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)PROD_SMEM));
+        attr = true;
+    }
+    k_product<TA, TB><<<grid, PNT, PROD_SMEM, st>>>(M, N, K, kchunk, A, lda, B, ldb, out, ldo,
+                                                    sstride, colmask, direct);
+    AERO_LAUNCHED();
+}
 }  // namespace
 
 size_t product_workspace_doubles(int M, int N) { return (size_t)8 * M * N; }
 
-void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
-                  int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles) {
-    if (M <= 0 || N <= 0) return;
-    static bool attr = false;
-    if (!attr) {
-        AERO_CUDA(cudaFuncSetAttribute(k_product, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(ProdSmem)));
-        attr = true;
-    }
+bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+              const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
+              size_t ws_doubles) {
+    if (M <= 0 || N <= 0) return true;
+    // 16-byte cp.async needs even leading dimensions and aligned bases
+    if ((lda & 1) || (ldb & 1) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15)) return false;
     const int tiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN);
-    // two resident CTAs per SM (2 x 77 KB shared memory): target 296 CTAs
     int splits = std::max(1, std::min(8, (296 + tiles / 2) / tiles));
     const int kt_total = (K + PBK - 1) / PBK;
     splits = std::min(splits, std::max(1, kt_total / 4));  // >= 4 K slices per split
-    if ((size_t)splits * M * N > ws_doubles) splits = 1;
+    if (!ws || (size_t)splits * M * N > ws_doubles) splits = 1;
     const int kchunk = ((kt_total + splits - 1) / splits) * PBK;
     dim3 grid((N + PBN - 1) / PBN, (M + PBM - 1) / PBM, splits);
-    if (splits == 1) {
-        k_product<<<grid, PNT, sizeof(ProdSmem), st>>>(M, N, K, kchunk, A, lda, B, ldb, Y, ldy, 0,
-                                                       colmask, 1);
-        AERO_LAUNCHED();
-        return;
-    }
     const int64_t sstride = (int64_t)M * N;
-    k_product<<<grid, PNT, sizeof(ProdSmem), st>>>(M, N, K, kchunk, A, lda, B, ldb, ws, M, sstride,
-                                                   nullptr, 0);
-    AERO_LAUNCHED();
-    const int64_t tot = (int64_t)M * N;
-    k_product_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, ws, sstride, Y,
-                                                                    ldy, colmask);
-    AERO_LAUNCHED();
+    double* o = splits == 1 ? Y : ws;
+    const int ldo = splits == 1 ? ldy : M;
+    const int direct = splits == 1;
+    if (!ta && !tb) launch<false, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
+    else if (ta && !tb) launch<true, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
+    else if (!ta && tb) launch<false, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
+    else launch<true, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
+    if (splits > 1) {
+        const int64_t tot = (int64_t)M * N;
+        k_product_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, ws, sstride, Y,
+                                                                        ldy, colmask);
+        AERO_LAUNCHED();
+    }
+    return true;
+}
+
+void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
+                  int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles) {
+    if (!gemm_big(st, false, false, M, N, K, A, lda, B, ldb, Y, ldy, colmask, ws, ws_doubles))
+        dgemm(st, false, false, M, N, K, 1.0, A, lda, B, ldb, 0.0, Y, ldy, colmask);
 }
 
 }  // namespace aero_b200

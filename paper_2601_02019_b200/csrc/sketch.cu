@@ -199,8 +199,10 @@ void Sketch::append_rows(const double* dev_rows, int64_t B) {
     const int r0 = r_;
     AERO_CUDA(cudaMemcpyAsync(C_.p + (size_t)r0 * d_, dev_rows, sizeof(double) * d_ * B,
                               cudaMemcpyDeviceToDevice, st_));
-    dgemm(st_, true, false, r0 + (int)B, (int)B, d_, 1.0, C_.p, d_, C_.p + (size_t)r0 * d_, d_,
-          0.0, G_.p + (size_t)r0 * cap_, cap_);
+    if (!gemm_big(st_, true, false, r0 + (int)B, (int)B, d_, C_.p, d_, C_.p + (size_t)r0 * d_, d_,
+                  G_.p + (size_t)r0 * cap_, cap_, nullptr, ws_.p, ws_.n))
+        dgemm(st_, true, false, r0 + (int)B, (int)B, d_, 1.0, C_.p, d_, C_.p + (size_t)r0 * d_, d_,
+              0.0, G_.p + (size_t)r0 * cap_, cap_);
     if (r0 > 0) {
         const int64_t tot = (int64_t)r0 * B;
         k_sym_fill<<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(r0, (int)B, G_.p, cap_);
@@ -223,10 +225,12 @@ void Sketch::reduce() {
     eigh(st_, n, E_.p, n, ew_.p);
     fd_weights(st_, ew_.p, n, ell_, keep, fw_.p);
     scale_columns(st_, n, keep, E_.p, n, fw_.p);
-    dgemm(st_, false, false, d_, keep, n, 1.0, C_.p, d_, E_.p, n, 0.0, C2_.p, d_);
+    if (!gemm_big(st_, false, false, d_, keep, n, C_.p, d_, E_.p, n, C2_.p, d_, nullptr, ws_.p, ws_.n))
+        dgemm(st_, false, false, d_, keep, n, 1.0, C_.p, d_, E_.p, n, 0.0, C2_.p, d_);
     std::swap(C_.p, C2_.p);
     std::swap(C_.n, C2_.n);
-    dgemm(st_, true, false, keep, keep, d_, 1.0, C_.p, d_, C_.p, d_, 0.0, G_.p, cap_);
+    if (!gemm_big(st_, true, false, keep, keep, d_, C_.p, d_, C_.p, d_, G_.p, cap_, nullptr, ws_.p, ws_.n))
+        dgemm(st_, true, false, keep, keep, d_, 1.0, C_.p, d_, C_.p, d_, 0.0, G_.p, cap_);
     r_ = keep;
     if (profiling) {
         AERO_CUDA(cudaEventRecord(ev_at(1), st_));
@@ -340,21 +344,27 @@ void Sketch::dump_from_job(int col, int k, int xi, int64_t t, double theta, bool
         AERO_LAUNCHED();
         fill_zero(st_, mt, tot);
     } else {
-        qy_.alloc((size_t)r * xi * 2 + (size_t)xi * xi + 64);
+        const int rl = r + (r & 1);  // even leading dimension (16-byte aligned columns)
+        qy_.alloc((size_t)rl * xi * 2 + (size_t)xi * xi + 64);
         double* HV = qy_.p;
-        double* P = HV + (size_t)r * xi;
-        double* ZZ = P + (size_t)r * xi;
+        double* P = HV + (size_t)rl * xi;
+        double* ZZ = P + (size_t)rl * xi;
         const double* vr = (k > 64) ? vr_.p : vr_.p + (size_t)col * kv_;
-        dgemm(st_, false, false, r, xi, k, 1.0, H_.p + (size_t)col * ldx_, ldx_, vr, k, 0.0, HV, r);
-        dgemm(st_, false, false, d_, xi, r, 1.0, C_.p, d_, HV, r, 0.0, z, d_);
+        auto big = [&](bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+                       const double* Bm, int ldb, double* Y, int ldy) {
+            if (!gemm_big(st_, ta, tb, M, N, K, A, lda, Bm, ldb, Y, ldy, nullptr, ws_.p, ws_.n))
+                dgemm(st_, ta, tb, M, N, K, 1.0, A, lda, Bm, ldb, 0.0, Y, ldy);
+        };
+        dgemm(st_, false, false, r, xi, k, 1.0, H_.p + (size_t)col * ldx_, ldx_, vr, k, 0.0, HV, rl);
+        big(false, false, d_, xi, r, C_.p, d_, HV, rl, z, d_);               // z = C'^T (H V)
         fix_column_signs(st_, d_, xi, z, d_, nullptr);
-        dgemm(st_, true, false, r, xi, d_, 1.0, C_.p, d_, z, d_, 0.0, P, r);      // P = C' z
-        dgemm(st_, false, false, d_, xi, r, 1.0, C_.p, d_, P, r, 0.0, mt, d_);     // m^T = C'^T P
-        dgemm(st_, false, true, d_, r, xi, -1.0, z, d_, P, r, 1.0, C_.p, d_);      // C' -= P z^T
-        dgemm(st_, true, false, xi, xi, d_, 1.0, z, d_, z, d_, 0.0, ZZ, xi);       // z^T z
+        big(true, false, r, xi, d_, C_.p, d_, z, d_, P, rl);                 // P = C' z
+        big(false, false, d_, xi, r, C_.p, d_, P, rl, mt, d_);               // m^T = C'^T P
+        dgemm(st_, false, true, d_, r, xi, -1.0, z, d_, P, rl, 1.0, C_.p, d_);  // C' -= P z^T
+        big(true, false, xi, xi, d_, z, d_, z, d_, ZZ, xi);                  // z^T z
         add_identity(st_, xi, ZZ, xi, -2.0);
-        dgemm(st_, false, false, r, xi, xi, 1.0, P, r, ZZ, xi, 0.0, HV, r);        // P (z^T z - 2I)
-        dgemm(st_, false, true, r, r, xi, 1.0, HV, r, P, r, 1.0, G_.p, cap_);
+        dgemm(st_, false, false, r, xi, xi, 1.0, P, rl, ZZ, xi, 0.0, HV, rl);   // P (z^T z - 2I)
+        dgemm(st_, false, true, r, r, xi, 1.0, HV, rl, P, rl, 1.0, G_.p, cap_);
         symmetrize(st_, r, G_.p, cap_);
     }
     SnapRec s{xi, last_dump_t_ + 1, t, theta, ch, ccol};
