@@ -447,6 +447,55 @@ class MlState:
         return out
 
 
+class CodState:
+    """reference CodState (amm.hpp:35-69): sliding-window AMM sketch."""
+
+    def __init__(self, dx, dy, eps, theta, n, seed=0, stream=0, device=0):
+        h = vp()
+        _chk(lib().aero_cod_create(dx, dy, eps, theta, n, seed, stream, device, C.byref(h)))
+        self._h, self.dx, self.dy = h, dx, dy
+        self.ell = self.info()["ell"]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_cod_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        ell, cols, ns, clock = i32(), i64(), i64(), i64()
+        _chk(lib().aero_cod_info(self._h, C.byref(ell), C.byref(cols), C.byref(ns), C.byref(clock)))
+        return dict(ell=ell.value, cols=cols.value, nsnaps=ns.value, clock=clock.value)
+
+    def update_block(self, xs, ys, ts):
+        xs, ys = _f64(xs), _f64(ys)
+        if xs.ndim != 2 or ys.ndim != 2 or xs.shape[1] != self.dx or ys.shape[1] != self.dy:
+            raise InvalidInput("CodState: dimension mismatch")
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = ts.shape[0]
+        ev = (Event * max(n, 1))()
+        _chk(lib().aero_cod_update_block(self._h, _dp(xs), _dp(ys), n, _lp(ts), ev))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
+
+    def update(self, x, y, i):
+        return self.update_block(np.asarray(x, np.float64)[None], np.asarray(y, np.float64)[None], [i])[0]
+
+    def query(self):
+        a, b = np.empty((self.dx, self.ell)), np.empty((self.dy, self.ell))
+        _chk(lib().aero_cod_query(self._h, _dp(a), _dp(b)))
+        return a, b
+
+    def query_product(self):
+        p = np.empty((self.dx, self.dy))
+        _chk(lib().aero_cod_query_product(self._h, _dp(p)))
+        return p
+
+
 def dist_theta_schedule(sq_norms, eps, latency=0):
     """Per-site thresholds from the norm-only protocol replay
     (distributed.cpp:31-69,107-123,201-239). sq_norms: (m, T)."""

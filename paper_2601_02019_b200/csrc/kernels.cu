@@ -616,6 +616,19 @@ void scale_columns(cudaStream_t st, int n, int ncol, double* V, int ld, const do
     AERO_LAUNCHED();
 }
 
+__global__ void k_scale_rows(int n, int ncol, double* V, int ld, const double* scale) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)n * ncol) return;
+    const int i = (int)(e % n), j = (int)(e / n);
+    V[i + (int64_t)j * ld] *= scale[i];
+}
+void scale_rows(cudaStream_t st, int n, int ncol, double* V, int ld, const double* scale) {
+    const int64_t tot = (int64_t)n * ncol;
+    if (tot <= 0) return;
+    k_scale_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, ncol, V, ld, scale);
+    AERO_LAUNCHED();
+}
+
 __global__ void k_fd_weights(const double* lam, int n, int ell, int keep, double* w) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= keep) return;

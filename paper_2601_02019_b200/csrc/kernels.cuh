@@ -71,6 +71,8 @@ void eigh_release();  // free cached solver handles/workspaces
 
 // columns of V (n x ncol, ld) scaled: V[:, i] *= scale[i]
 void scale_columns(cudaStream_t st, int n, int ncol, double* V, int ld, const double* scale);
+// rows scaled: V[i, :] *= scale[i]
+void scale_rows(cudaStream_t st, int n, int ncol, double* V, int ld, const double* scale);
 // FD reduce weights (fd.cpp:20-27 via eig of C'C'^T): from eigenvalues lam
 // (descending) compute w_i = sqrt(s2_i)/sigma_i with sigma_i = sqrt(max(lam,0)),
 // s2_i = sigma_i^2 - sigma_{ell-1}^2 (0 if <= 0), for i < keep

@@ -333,3 +333,52 @@ def test_kernels_launched():
     s = prod.AttpState(64, 0.25, seed=1)
     s.update_block(np.random.default_rng(1).standard_normal((50, 64)), np.arange(1, 51))
     assert prod.kernel_launches() > n0
+
+
+# ---------------------------------------------------------------- amm (CodState)
+def test_cod_kats():  # test_amm.cpp:48-102
+    s = prod.CodState(4, 4, 1.0, 1.0, 100, seed=2)
+    v = 10.0 * np.eye(4)[0]
+    s.update(v, v, 1)
+    assert s.info()["nsnaps"] == 1
+    p = s.query_product()
+    assert np.linalg.norm(p - np.outer(v, v)) / 100.0 < 1e-8
+    s = prod.CodState(4, 4, 1.0, 1.0, 5, seed=3)
+    s.update(v, v, 1)
+    for i in range(2, 7):
+        s.update(0.01 * np.ones(4), 0.01 * np.ones(4), i)
+    assert s.info()["nsnaps"] == 0
+    a, b = s.query()
+    assert (a @ b.T)[0, 0] < 1.0
+    s = prod.CodState(5, 3, 0.5, 1.0, 10, seed=4)
+    with pytest.raises(prod.InvalidInput):
+        s.update(np.ones(3), np.ones(3), 1)
+    s.update(np.ones(5), np.ones(3), 1)
+    with pytest.raises(prod.InvalidInput):
+        s.update(np.ones(5), np.ones(3), 1)
+
+
+@pytest.mark.parametrize("dx,dy,n,eps,T", [(8, 6, 100, 0.25, 300), (24, 16, 400, 0.2, 700),
+                                           (64, 48, 300, 1 / 16, 500)])
+def test_cod_parity(orc, dx, dy, n, eps, T):
+    """CodState (amm.cpp:42-122) against the oracle: identical decision trace,
+    restored product within 1e-8, window error within the budget."""
+    ref = orc.CodState(dx, dy, eps, eps * n, n, 8, 1000)
+    s = prod.CodState(dx, dy, eps, eps * n, n, seed=8, stream=1000)
+    xs, ys = uniform_rows(orc, T, dx, 8, 0), uniform_rows(orc, T, dy, 8, 1)
+    for b in range(0, T, 100):
+        ts = np.arange(b + 1, b + 101)
+        ev_ref = ref.update_block(xs[b:b + 100], ys[b:b + 100], ts)
+        ev = s.update_block(xs[b:b + 100], ys[b:b + 100], ts)
+        assert_trace_equal(ev, ev_ref, rtol=1e-7)
+        pr, pg = ref.query_product(), s.query_product()
+        assert rel_fro(pg, pr) < 1e-8
+        i = b + 100
+        lo = max(0, i - n)
+        p = xs[lo:i].T @ ys[lo:i]
+        den = math.sqrt(np.sum(xs[lo:i] ** 2) * np.sum(ys[lo:i] ** 2))
+        a, bb = s.query()
+        e_gpu = orc.spectral_norm(p - a @ bb.T) / den
+        ar, br = ref.query()
+        e_ref = orc.spectral_norm(p - ar @ br.T) / den
+        assert abs(e_gpu - e_ref) < 1e-6 and (e_gpu <= eps or e_ref > eps)
