@@ -163,6 +163,18 @@ int aero_ml_heavy_get(aero_ml* h, int32_t level, int64_t idx, double* row, int64
 int aero_dist_theta_schedule(int32_t m, int64_t T, double eps, int64_t latency,
                              const double* sq_norms, double* theta_out, int64_t* mass_bytes,
                              int64_t* broadcasts);
+/* the same replay, streaming: state persists across calls; advance() consumes
+ * the next T ticks of every site's squared norms (m x T row-major) */
+typedef struct aero_dist_protocol aero_dist_protocol;
+int aero_dist_protocol_create(int32_t m, double eps, int64_t latency, aero_dist_protocol** out);
+int aero_dist_protocol_destroy(aero_dist_protocol* h);
+int aero_dist_protocol_advance(aero_dist_protocol* h, int64_t T, const double* sq_norms,
+                               double* theta_out);
+int aero_dist_protocol_info(aero_dist_protocol* h, int64_t* ticks, int64_t* mass_bytes,
+                            int64_t* broadcasts, double* f_hat);
+/* squared norms of n device rows (row-major, ld) into host memory (K1) */
+int aero_row_sq_norms_device(const double* rows_device, int64_t n, int64_t ld, int32_t d,
+                             int32_t device, double* out_host);
 typedef struct aero_coord aero_coord;
 /* coordinator accumulator B (d x d fp64) on `device`; nccl_comm is an
  * ncclComm_t (or NULL for single-process use) */

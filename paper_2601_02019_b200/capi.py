@@ -134,6 +134,11 @@ SIGNATURES = [
     ("aero_ml_heavy_count", i32, [vp, i32, P(i64)]),
     ("aero_ml_heavy_get", i32, [vp, i32, i64, P(f64), P(i64), P(i64)]),
     ("aero_dist_theta_schedule", i32, [i32, i64, f64, i64, P(f64), P(f64), P(i64), P(i64)]),
+    ("aero_dist_protocol_create", i32, [i32, f64, i64, P(vp)]),
+    ("aero_dist_protocol_destroy", i32, [vp]),
+    ("aero_dist_protocol_advance", i32, [vp, i64, P(f64), P(f64)]),
+    ("aero_dist_protocol_info", i32, [vp, P(i64), P(i64), P(i64), P(f64)]),
+    ("aero_row_sq_norms_device", i32, [vp, i64, i64, i32, i32, P(f64)]),
     ("aero_coord_create", i32, [i32, i32, i32, vp, P(vp)]),
     ("aero_coord_destroy", i32, [vp]),
     ("aero_coord_absorb_snapshots", i32, [vp, vp, P(i64)]),
@@ -505,6 +510,48 @@ def dist_theta_schedule(sq_norms, eps, latency=0):
     mb, bc = i64(), i64()
     _chk(lib().aero_dist_theta_schedule(m, T, eps, latency, _dp(sq), _dp(th), C.byref(mb), C.byref(bc)))
     return th, mb.value, bc.value
+
+
+class DistProtocol:
+    """Streaming norm-only replay of the whole-stream mass protocol
+    (distributed.cpp:31-69, 107-123, 201-239): per-site thresholds per tick."""
+
+    def __init__(self, m, eps, latency=0):
+        h = vp()
+        _chk(lib().aero_dist_protocol_create(m, eps, latency, C.byref(h)))
+        self._h, self.m = h, m
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_dist_protocol_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def advance(self, sq_norms):
+        sq = _f64(sq_norms)
+        if sq.ndim != 2 or sq.shape[0] != self.m:
+            raise InvalidInput("protocol: norms must be (m, T)")
+        th = np.empty_like(sq)
+        _chk(lib().aero_dist_protocol_advance(self._h, sq.shape[1], _dp(sq), _dp(th)))
+        return th
+
+    def info(self):
+        t, b, bc, fh = i64(), i64(), i64(), f64()
+        _chk(lib().aero_dist_protocol_info(self._h, C.byref(t), C.byref(b), C.byref(bc), C.byref(fh)))
+        return dict(ticks=t.value, mass_bytes=b.value, broadcasts=bc.value, f_hat=fh.value)
+
+
+def row_sq_norms_device(rows, device=0):
+    """Squared row norms of a CUDA (n, d) float64 tensor (the K1 kernel)."""
+    ptr, ld = _device_ptr(rows)
+    out = np.empty(rows.shape[0])
+    _chk(lib().aero_row_sq_norms_device(ptr, rows.shape[0], ld, rows.shape[1], device, _dp(out)))
+    return out
 
 
 class Coordinator:

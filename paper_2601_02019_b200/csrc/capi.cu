@@ -299,6 +299,54 @@ int aero_dist_theta_schedule(int32_t m, int64_t T, double eps, int64_t latency,
         dist_theta_schedule(m, T, eps, latency, sq_norms, theta_out, mass_bytes, broadcasts);
     });
 }
+struct aero_dist_protocol {
+    DistProtocol* p;
+};
+int aero_dist_protocol_create(int32_t m, double eps, int64_t latency, aero_dist_protocol** out) {
+    REQ(out);
+    return guard([&] { *out = new aero_dist_protocol{new DistProtocol(m, eps, latency)}; });
+}
+int aero_dist_protocol_destroy(aero_dist_protocol* h) {
+    if (!h) return AERO_OK;
+    delete h->p;
+    delete h;
+    return AERO_OK;
+}
+int aero_dist_protocol_advance(aero_dist_protocol* h, int64_t T, const double* sq_norms,
+                               double* theta_out) {
+    REQ(h);
+    if (T > 0) {
+        REQ(sq_norms);
+        REQ(theta_out);
+    }
+    return guard([&] { h->p->advance(T, sq_norms, theta_out); });
+}
+int aero_dist_protocol_info(aero_dist_protocol* h, int64_t* ticks, int64_t* mass_bytes,
+                            int64_t* broadcasts, double* f_hat) {
+    REQ(h);
+    if (ticks) *ticks = h->p->ticks;
+    if (mass_bytes) *mass_bytes = h->p->bytes;
+    if (broadcasts) *broadcasts = h->p->broadcasts;
+    if (f_hat) *f_hat = h->p->f_hat;
+    return AERO_OK;
+}
+int aero_row_sq_norms_device(const double* rows_device, int64_t n, int64_t ld, int32_t d,
+                             int32_t device, double* out_host) {
+    REQ(rows_device);
+    REQ(out_host);
+    return guard([&] {
+        AERO_CUDA(cudaSetDevice(device));
+        double* nrm = nullptr;
+        int* bad = nullptr;
+        AERO_CUDA(cudaMalloc(&nrm, sizeof(double) * std::max<int64_t>(n, 1)));
+        AERO_CUDA(cudaMalloc(&bad, sizeof(int) * std::max<int64_t>(n, 1)));
+        ingest_rows(0, rows_device, n, ld, d, nrm, bad);
+        AERO_CUDA(cudaMemcpy(out_host, nrm, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        cudaFree(nrm);
+        cudaFree(bad);
+    });
+}
+
 struct aero_coord {
     Coordinator* c;
 };

@@ -296,46 +296,57 @@ void MlEngine::heavy_get(int j, int64_t idx, double* row, int64_t* s, int64_t* t
 // for the site side, :107-123 for the coordinator, :201-239 for the tick loop
 // and FIFO latencies). Snapshot messages ride the same FIFO but never change
 // the mass estimate, so every site's threshold is a function of norms alone.
-void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const double* sq_norms,
-                         double* theta_out, int64_t* mass_bytes, int64_t* broadcasts) {
+DistProtocol::DistProtocol(int m, double eps, int64_t latency)
+    : m_(m), eps_(eps), latency_(latency), f_local_(m > 0 ? m : 0, 0.0),
+      f_self_(m > 0 ? m : 0, 0.0), f_known_(m > 0 ? m : 0, 0.0) {
     if (m < 1) throw InvalidInput("run_simulation: m must be >= 1");
     if (!(eps > 0.0 && eps <= 1.0)) throw InvalidInput("run_simulation: eps out of (0,1]");
-    std::vector<double> f_local(m, 0.0), f_self(m, 0.0), f_known(m, 0.0);
-    double f_hat = 0.0;
-    int msg_count = 0;
-    int64_t bc = 0, bytes = 0;
-    std::deque<std::pair<int64_t, double>> to_coord, to_sites;
-    for (int64_t i = 1; i <= T; ++i) {
-        while (!to_sites.empty() && to_sites.front().first <= i) {
-            for (int j = 0; j < m; ++j) f_known[j] = std::max(f_known[j], to_sites.front().second);
-            to_sites.pop_front();
+    if (latency < 0) throw InvalidInput("run_simulation: latency must be >= 0");
+}
+
+// ticks ticks+1 .. ticks+T; site j's norms at sq_norms[j * T + q]
+void DistProtocol::advance(int64_t T, const double* sq_norms, double* theta_out) {
+    const int m = m_;
+    const double eps = eps_;
+    for (int64_t q = 0; q < T; ++q) {
+        const int64_t i = ticks + q + 1;
+        while (!to_sites_.empty() && to_sites_.front().first <= i) {  // distributed.cpp:211-215
+            for (int j = 0; j < m; ++j) f_known_[j] = std::max(f_known_[j], to_sites_.front().second);
+            to_sites_.pop_front();
         }
-        for (int j = 0; j < m; ++j) {
-            const double nsq = sq_norms[(int64_t)j * T + (i - 1)];
-            f_local[j] += nsq;
-            if (f_local[j] >= (eps / m) * f_known[j]) {
-                to_coord.emplace_back(i + latency, f_local[j]);
+        for (int j = 0; j < m; ++j) {  // SiteState::update, distributed.cpp:57-69
+            const double nsq = sq_norms[(int64_t)j * T + q];
+            f_local_[j] += nsq;
+            if (f_local_[j] >= (eps / m) * f_known_[j]) {
+                to_coord_.emplace_back(i + latency_, f_local_[j]);
                 bytes += 8 + 16;
-                f_self[j] += f_local[j];
-                f_local[j] = 0.0;
+                f_self_[j] += f_local_[j];
+                f_local_[j] = 0.0;
             }
-            theta_out[(int64_t)j * T + (i - 1)] = eps * std::max(f_known[j], f_self[j] + f_local[j]);
+            theta_out[(int64_t)j * T + q] = eps * std::max(f_known_[j], f_self_[j] + f_local_[j]);
         }
-        while (!to_coord.empty() && to_coord.front().first <= i) {
-            const double f = to_coord.front().second;
-            to_coord.pop_front();
+        while (!to_coord_.empty() && to_coord_.front().first <= i) {  // distributed.cpp:231-239
+            const double f = to_coord_.front().second;
+            to_coord_.pop_front();
             if (!(f >= 0.0)) throw ProtocolError("FroMass: negative mass");
-            f_hat = std::max(f_hat + f, 0.0);
-            if (++msg_count >= m) {
-                msg_count = 0;
-                ++bc;
+            f_hat = std::max(f_hat + f, 0.0);  // CoordinatorState::receive, :109-123
+            if (++msg_count_ >= m) {
+                msg_count_ = 0;
+                ++broadcasts;
                 bytes += (int64_t)m * (8 + 16);
-                to_sites.emplace_back(i + 1 + latency, f_hat);
+                to_sites_.emplace_back(i + 1 + latency_, f_hat);
             }
         }
     }
-    if (mass_bytes) *mass_bytes = bytes;
-    if (broadcasts) *broadcasts = bc;
+    ticks += T;
+}
+
+void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const double* sq_norms,
+                         double* theta_out, int64_t* mass_bytes, int64_t* broadcasts) {
+    DistProtocol p(m, eps, latency);
+    p.advance(T, sq_norms, theta_out);
+    if (mass_bytes) *mass_bytes = p.bytes;
+    if (broadcasts) *broadcasts = p.broadcasts;
 }
 
 Coordinator::Coordinator(int d, int m, int device, void* comm) : d_(d), m_(m), dev_(device), comm_(comm) {

@@ -51,6 +51,22 @@ class MlEngine {
 // ---- distributed (distributed.cpp:31-173) ---------------------------------
 void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const double* sq_norms,
                          double* theta_out, int64_t* mass_bytes, int64_t* broadcasts);
+// streaming form of the replay (state persists across advance() calls)
+class DistProtocol {
+  public:
+    DistProtocol(int m, double eps, int64_t latency);
+    void advance(int64_t T, const double* sq_norms, double* theta_out);
+    int64_t ticks = 0, bytes = 0, broadcasts = 0;
+    double f_hat = 0.0;
+
+  private:
+    int m_;
+    double eps_;
+    int64_t latency_;
+    std::vector<double> f_local_, f_self_, f_known_;
+    int msg_count_ = 0;
+    std::deque<std::pair<int64_t, double>> to_coord_, to_sites_;
+};
 class Coordinator {
   public:
     Coordinator(int d, int m, int device, void* nccl_comm);

@@ -382,3 +382,24 @@ def test_cod_parity(orc, dx, dy, n, eps, T):
         ar, br = ref.query()
         e_ref = orc.spectral_norm(p - ar @ br.T) / den
         assert abs(e_gpu - e_ref) < 1e-6 and (e_gpu <= eps or e_ref > eps)
+
+
+def test_distributed_sketch_nccl_merge(orc):
+    """DistributedSketch with the NCCL merge path (single-rank communicator on
+    the one GPU): probe errors and protocol bytes against the oracle simulator."""
+    from paper_2601_02019_b200.distributed import DistributedSketch
+    m, d, eps, T, qe = 4, 32, 0.2, 600, 100
+    streams = np.stack([uniform_rows(orc, T, d, 3, j) for j in range(m)])
+    ref = orc.dist_run(streams, eps, query_every=qe, seed=3)
+    ds = DistributedSketch(d, eps, m, seed=3, use_nccl=True)
+    g = orc.OracleGram(d)
+    errs = []
+    for b in range(0, T, qe):
+        ds.ingest({j: streams[j, b:b + qe] for j in range(m)}, b + 1)
+        for j in range(m):
+            g.add_block(streams[j, b:b + qe], np.arange(b + 1, b + qe + 1))
+        sk, gram = ds.probe(want_gram=True)
+        errs.append(g.error(sk))
+    assert ds.exchange.mass_bytes + ds.snapshot_bytes == ref["comm_bytes"]
+    assert np.max(np.abs(np.array(errs) - ref["probe_err"])) <= 1e-6
+    assert rel_fro(gram, ref["last_probe_gram"]) < 1e-9
