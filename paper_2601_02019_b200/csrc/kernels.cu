@@ -385,8 +385,9 @@ void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G,
 
 // k x k Gram of two column blocks P (r x k) and Q (r x k), ld, into S (smem, col-major)
 template <int KM>
-__device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k, double* S,
-                         double* red) {
+__device__ void cta_gram(const double* P, int ldp, const double* Q, int ldq, int r, int k,
+                         double* S, double* red) {
+    const int ld = ldp;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int E = k * k;
     if (KM <= 4) {
@@ -398,8 +399,8 @@ __device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k,
             double p[KM], q[KM];
 #pragma unroll
             for (int a = 0; a < KM; ++a) {
-                p[a] = (a < k) ? P[i + (int64_t)a * ld] : 0.0;
-                q[a] = (a < k) ? Q[i + (int64_t)a * ld] : 0.0;
+                p[a] = (a < k) ? P[i + (int64_t)a * ldp] : 0.0;
+                q[a] = (a < k) ? Q[i + (int64_t)a * ldq] : 0.0;
             }
 #pragma unroll
             for (int a = 0; a < KM; ++a)
@@ -425,7 +426,7 @@ __device__ void cta_gram(const double* P, const double* Q, int ld, int r, int k,
         for (int e = tid; e < E; e += nt) {
             const int a = e % k, b = e / k;
             double t = 0.0;
-            for (int i = 0; i < r; ++i) t = fma(P[i + (int64_t)a * ld], Q[i + (int64_t)b * ld], t);
+            for (int i = 0; i < r; ++i) t = fma(P[i + (int64_t)a * ld], Q[i + (int64_t)b * ldq], t);
             S[e] = t;
         }
         __syncthreads();
@@ -463,11 +464,15 @@ __device__ void small_eig(double* W, double* T, int k, double* cs) {
     __syncthreads();
 }
 
-template <int KM>
+// WS: Y arrives as `splits` split-K partials in ws (ws[z*sstride + i + c*wsM]),
+// summed here in fixed order into shared memory (fuses k_product_reduce)
+template <int KM, bool WS>
 __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, double* X,
                                  const double* __restrict__ Y, int ldx, double* H,
                                  int* __restrict__ status, double* __restrict__ out_sig,
-                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped) {
+                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
+                                 const double* __restrict__ ws, int wsM, int64_t sstride,
+                                 int splits) {
     extern __shared__ double sm[];
     const IterJob jb = jobs[blockIdx.x];
     if (phase >= jb.nphase) return;
@@ -476,13 +481,13 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     const int tid = threadIdx.x, nt = blockDim.x;
     const int r = jb.r, k = jb.k;
     double* x = X + (int64_t)jb.col * ldx;
-    const double* y = Y + (int64_t)jb.col * ldx;
     double* red = sm;                  // 32*16
     double* S = red + 32 * 16;         // KM*KM
     double* W = S + KM * KM;           // KM*KM
     double* T = W + KM * KM;           // KM*KM
     double* lam = T + KM * KM;         // KM
     double* cs = lam + KM;             // jacobi scratch
+    double* ysh = cs + jacobi_scratch_doubles(KM);  // WS: r * k
     if (st != JOB_ACTIVE) {
         if (last && tid == 0) {
             if (jb.type == 0) out_sig[jb.col] = 0.0;
@@ -490,6 +495,23 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
                 for (int a = 0; a < k; ++a) out_sig[jb.col + a] = 0.0;
         }
         return;
+    }
+    const double* y;
+    int ldy;
+    if (WS) {
+        for (int e = tid; e < r * k; e += nt) {
+            const int i = e % r, a = e / r;
+            const double* p = ws + i + (int64_t)(jb.col + a) * wsM;
+            double v = 0.0;
+            for (int z = 0; z < splits; ++z) v += p[z * sstride];
+            ysh[e] = v;
+        }
+        __syncthreads();
+        y = ysh;
+        ldy = r;
+    } else {
+        y = Y + (int64_t)jb.col * ldx;
+        ldy = ldx;
     }
     if (jb.type == 0) {
         if (!last) {
@@ -511,7 +533,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
         return;
     }
     // simul: S = X^T Y (Gram of g = C'^T X), T = S^{-1/2}
-    cta_gram<KM>(x, y, ldx, r, k, S, red);
+    cta_gram<KM>(x, ldx, y, ldy, r, k, S, red);
     for (int e = tid; e < k * k; e += nt) {
         const int a = e % k, b = e / k;
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
@@ -541,7 +563,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
         for (int a = 0; a < KM; ++a) {
             if (a < k) {
                 xr[a] = x[i + (int64_t)a * ldx];
-                yr[a] = y[i + (int64_t)a * ldx];
+                yr[a] = y[i + (int64_t)a * ldy];
             }
         }
 #pragma unroll
@@ -562,7 +584,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     __syncthreads();
     if (!last) return;
     // Ritz values: eig(w^T w), w = C' g = G H = X (linalg.cpp:145-150)
-    cta_gram<KM>(x, x, ldx, r, k, S, red);
+    cta_gram<KM>(x, ldx, x, ldx, r, k, S, red);
     for (int e = tid; e < k * k; e += nt) {
         const int a = e % k, b = e / k;
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
@@ -574,17 +596,19 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
     for (int a = tid; a < k; a += nt) out_sig[jb.col + a] = sqrt(fmax(lam[a], 0.0));
 }
 
-template <int KM>
+template <int KM, bool WS>
 static void launch_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
                              const double* Y, int ldx, double* H, int* status, double* out_sig,
-                             double* out_vr, int kv, int* out_clamped) {
-    const size_t smem =
-        sizeof(double) * (32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM)) + 16;
+                             double* out_vr, int kv, int* out_clamped, const double* ws, int wsM,
+                             int64_t sstride, int splits) {
+    const size_t smem = sizeof(double) * (32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM) +
+                                          (WS ? (size_t)wsM * KM : 0)) + 16;
     if (smem > 48 * 1024)
-        AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    k_iter_normalize<KM><<<njobs, 256, smem, st>>>(jobs, phase, X, Y, ldx, H, status, out_sig, out_vr,
-                                                   kv, out_clamped);
+        AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize<KM, WS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_iter_normalize<KM, WS><<<njobs, 256, smem, st>>>(jobs, phase, X, Y, ldx, H, status, out_sig,
+                                                       out_vr, kv, out_clamped, ws, wsM, sstride,
+                                                       splits);
     AERO_LAUNCHED();
 }
 
@@ -593,11 +617,27 @@ void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, 
                     double* out_vr, int kv, int* out_clamped, int max_k) {
     if (njobs <= 0) return;
     if (max_k <= 2)
-        launch_normalize<2>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+        launch_normalize<2, false>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv,
+                                   out_clamped, nullptr, 0, 0, 0);
     else if (max_k <= 4)
-        launch_normalize<4>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+        launch_normalize<4, false>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv,
+                                   out_clamped, nullptr, 0, 0, 0);
     else
-        launch_normalize<64>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+        launch_normalize<64, false>(st, jobs, njobs, phase, X, Y, ldx, H, status, out_sig, out_vr, kv,
+                                    out_clamped, nullptr, 0, 0, 0);
+}
+
+void iter_normalize_ws(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
+                       int ldx, const double* ws, int M, int N, int splits, double* H, int* status,
+                       double* out_sig, double* out_vr, int kv, int* out_clamped, int max_k) {
+    if (njobs <= 0) return;
+    const int64_t sstride = (int64_t)M * N;
+    if (max_k <= 2)
+        launch_normalize<2, true>(st, jobs, njobs, phase, X, nullptr, ldx, H, status, out_sig, out_vr,
+                                  kv, out_clamped, ws, M, sstride, splits);
+    else
+        launch_normalize<4, true>(st, jobs, njobs, phase, X, nullptr, ldx, H, status, out_sig, out_vr,
+                                  kv, out_clamped, ws, M, sstride, splits);
 }
 
 // ============================================================================

@@ -21,9 +21,11 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha,
 size_t product_workspace_doubles(int M, int N);
 // Y = op(A) op(B) on the fast path (alpha = 1, beta = 0); returns false (and
 // does nothing) when operand alignment rules it out -- callers then use dgemm
+// (defer_reduce: leave split-K partials in ws, ws[z*M*N + i + j*M], and report
+// the split count; the caller's consumer sums them -- iter_normalize_ws)
 bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
               const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
-              size_t ws_doubles);
+              size_t ws_doubles, int* splits_used = nullptr, bool defer_reduce = false);
 void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
                   int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles);
 
@@ -57,6 +59,12 @@ void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G,
 void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
                     const double* Y, int ldx, double* H, int* status, double* out_sig,
                     double* out_vr, int kv, int* out_clamped, int max_k);
+// same, with Y given as `splits` split-K partials of an M x N product in ws
+// (summed in fixed order per job, cached in shared memory): fuses the split-K
+// reduction into the normalization (k <= 4)
+void iter_normalize_ws(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
+                       int ldx, const double* ws, int M, int N, int splits, double* H, int* status,
+                       double* out_sig, double* out_vr, int kv, int* out_clamped, int max_k);
 
 // ---- small dense helpers ---------------------------------------------------
 // symmetric eigendecomposition of `batch` n x n matrices (column-major, ld,

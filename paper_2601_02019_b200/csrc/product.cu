@@ -180,7 +180,7 @@ size_t product_workspace_doubles(int M, int N) { return (size_t)8 * M * N; }
 
 bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
               const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
-              size_t ws_doubles) {
+              size_t ws_doubles, int* splits_used, bool defer_reduce) {
     if (M <= 0 || N <= 0) return true;
     // 16-byte cp.async needs even leading dimensions and aligned bases
     if ((lda & 1) || (ldb & 1) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15)) return false;
@@ -199,7 +199,8 @@ bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const doub
     else if (ta && !tb) launch<true, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
     else if (!ta && tb) launch<false, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
     else launch<true, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
-    if (splits > 1) {
+    if (splits_used) *splits_used = splits;
+    if (splits > 1 && !defer_reduce) {
         const int64_t tot = (int64_t)M * N;
         k_product_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, ws, sstride, Y,
                                                                         ldy, colmask);

@@ -90,7 +90,8 @@ Sketch::Sketch(const aero_cfg& cfg) {
     cap_ = 2 * ell_;
     kp_ = power_iter_count(d_);
     q_ = simul_q(d_, eps_si_);
-    max_batch_ = cfg.max_batch > 0 ? cfg.max_batch : 64;
+    max_batch_ = cfg.max_batch > 0 ? cfg.max_batch : 192;
+    cur_batch_ = std::min(64, max_batch_);
     AERO_CUDA(cudaSetDevice(dev_));
     AERO_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     C_.alloc((size_t)d_ * cap_);
@@ -263,15 +264,27 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
                 flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
             }
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2 + 2 * p), st_));
-        gemm_product(st_, R, ncol, R, G_.p, cap_, X_.p, ldx_, Y_.p, ldx_, colmask_d_, ws_.p, ws_.n);
+        // (fusing the split-K sum into the per-job normalization measured slower:
+        // one CTA per job streams all partials -- profiles/round1_c2_steady_launches.txt)
+        constexpr bool kFuseSplitK = false;
+        int splits = 1;
+        const bool fast = gemm_big(st_, false, false, R, ncol, R, G_.p, cap_, X_.p, ldx_, Y_.p,
+                                   ldx_, colmask_d_, ws_.p, ws_.n, &splits, kFuseSplitK && max_k <= 4);
+        if (!fast)
+            dgemm(st_, false, false, R, ncol, R, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_,
+                  colmask_d_);
         if (profiling) {
             AERO_CUDA(cudaEventRecord(ev_at(3 + 2 * p), st_));
             prof.product_launches++;
             prof.product_flops += flops;
             prof.product_bytes += 8.0 * ((double)R * R + 2.0 * (double)R * ncol);
         }
-        iter_normalize(st_, jobs_d_, njobs, p, X_.p, Y_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p,
-                       kv_, clamp_d_, std::max(max_k, 1));
+        if (kFuseSplitK && fast && splits > 1 && max_k <= 4)  // split-K sum fused into the normalization
+            iter_normalize_ws(st_, jobs_d_, njobs, p, X_.p, ldx_, ws_.p, R, ncol, splits, H_.p,
+                              status_d_, sig_.p, vr_.p, kv_, clamp_d_, std::max(max_k, 1));
+        else
+            iter_normalize(st_, jobs_d_, njobs, p, X_.p, Y_.p, ldx_, H_.p, status_d_, sig_.p,
+                           vr_.p, kv_, clamp_d_, std::max(max_k, 1));
     }
     if (profiling) AERO_CUDA(cudaEventRecord(ev_at(1), st_));
     AERO_CUDA(cudaMemcpyAsync(sig_h_, sig_.p, sizeof(double) * ncol_total, cudaMemcpyDeviceToHost, st_));
@@ -583,8 +596,19 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
             pos++;
             continue;
         }
-        const int64_t B = std::min<int64_t>({(int64_t)max_batch_, n - pos, room});
-        pos += run_batch(dev_rows + (size_t)pos * d_, B, t + pos, thetas + pos, log + pos);
+        // batch size from the observed rate p of batch-ending rows: a batch
+        // costs ~alpha + beta*B (alpha = the fixed phase latency, ~40 rows'
+        // worth of products) and commits (1-(1-p)^B)/p rows on average, which
+        // is cheapest per row near B* = sqrt(2 alpha / (beta p))
+        const double p = std::max(end_rate_, 1e-4);
+        cur_batch_ = (int)std::clamp(std::sqrt(52.0 / p), 16.0, (double)max_batch_);
+        const int64_t B = std::min<int64_t>({(int64_t)cur_batch_, n - pos, room});
+        const int64_t mp0 = mispredicts;
+        const int64_t used = run_batch(dev_rows + (size_t)pos * d_, B, t + pos, thetas + pos, log + pos);
+        const double ended = (mispredicts > mp0) ? 1.0 : 0.0;
+        const double w = std::min(1.0, (double)used / 256.0);  // EMA over ~256 rows
+        end_rate_ = (1.0 - w) * end_rate_ + w * (ended / (double)used);
+        pos += used;
     }
     if (n > 0) last_ev_ = log[n - 1];
 }

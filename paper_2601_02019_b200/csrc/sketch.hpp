@@ -105,7 +105,7 @@ class Sketch {
     void ensure_query_buffers();
 
     // config
-    int d_, ell_, cap_, kp_, q_, mode_, max_batch_;
+    int d_, ell_, cap_, kp_, q_, mode_, max_batch_, cur_batch_ = 64;
     bool exact_;
     std::vector<cudaEvent_t> ev_pool_;
     cudaEvent_t evA_ = nullptr, evB_ = nullptr;
@@ -120,7 +120,8 @@ class Sketch {
     uint64_t forks_ = 0;
     int r_ = 0;
     Pattern pattern_ = FIRE1;
-    double fire_ema_ = 1.0;  // moving average of gate fires (batch prediction)
+    double fire_ema_ = 1.0;   // moving average of gate fires (batch prediction)
+    double end_rate_ = 0.01;  // moving average of batch-ending rows per row (batch size)
     std::deque<SnapRec> snaps_;
     std::deque<Chunk*> chunks_;
     aero_event last_ev_{};

@@ -8,6 +8,6 @@ timeout 900 $CMD > $OUT/steady_plain.log 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s 150000 -c 6000 --csv \
     --log-file $OUT/steady_launches.csv $CMD > $OUT/steady_ncu_launches.log 2>&1
 echo "launch list rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'k_product<0' -s 30000 -c 3 \
-    -o $OUT/steady_prof $CMD > $OUT/steady_ncu_full.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_product \
+    -s ${KSKIP:-24000} -c ${KCOUNT:-6} -o $OUT/steady_prof $CMD > $OUT/steady_ncu_full.log 2>&1
 echo "full rc=$?"
