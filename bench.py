@@ -33,6 +33,15 @@ CONFIGS = {
                rows_per_step=8192, cpu_rows=400,
                name="C2 tight-eps persistent stream n=1048576 d=4096 eps=1/512 "
                     "(k=256, sigma=0.99^j, noise 0.05, R=256)"),
+    "c3": dict(kind="sw", d=1024, eps=1 / 64, k=64, rho=0.9, noise=0.1, r_max=1024.0, n=1048576,
+               window=65536, drift=131072, rows_per_step=4096, cpu_rows=600,
+               name="C3 sliding window N=65536 n=1048576 d=1024 eps=1/64 R=1024 (k=64, drift 131072)"),
+    "c4": dict(kind="dist", d=2048, eps=1 / 128, k=128, rho=0.97, noise=0.1, r_max=64.0, n=1048576,
+               k2=16, rho2=0.9, scale2=0.5, rows_per_step=4096, cpu_rows=300,
+               name="C4 distributed, one site per GPU, d=2048 eps=1/128 (global k=128 + site k=16, noise 0.1, R=64)"),
+    "c5": dict(kind="amm", dx=1024, dy=768, d=1024, eps=1 / 64, latent=48, noise=0.1, r_max=64.0,
+               n=1048576, window=65536, rows_per_step=512, cpu_rows=200,
+               name="C5 sliding-window AMM dx=1024 dy=768 N=65536 eps=1/64 (latent 48, noise 0.1)"),
 }
 
 
@@ -137,6 +146,22 @@ def run_reference(args, cfg, rank):
     import numpy as np
     threads = os.cpu_count() or 1
     orc.set_threads(threads)
+    if cfg["kind"] != "attp":
+        sites = args.gpus if cfg["kind"] == "dist" else 1
+        n = max(20, (args.cpu_rows or cfg["cpu_rows"]) // sites)
+        v, _ = cpu_other_rate(cfg, n, threads, sites=sites)
+        unit = "row-site updates/s" if cfg["kind"] == "dist" else "rows/s"
+        print(json.dumps({
+            "impl": "reference", "metric": "sketch update throughput", "value": v, "unit": unit,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": n * 1e3 / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "rows_per_step": n},
+            "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "port",
+                             "sample": f"rows 1..{n} of {args.config.upper()} ({sites} site(s)) from an empty state"},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     per = max(1, (args.cpu_rows or cfg["cpu_rows"]) // max(1, args.steps + args.warmup))
     nrows = per * (args.steps + args.warmup)
     rows = orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, 0, 1, nrows)
@@ -160,6 +185,133 @@ def run_reference(args, cfg, rank):
     }), flush=True)
 
 
+def oracle_stream(cfg, nrows, stream=0):
+    """Host rows of the config generator (oracle restatement, CPU baseline only)."""
+    from oracle import pyoracle as orc
+    if cfg["kind"] == "amm":
+        return orc.gen_amm_rows(1, cfg["dx"], cfg["dy"], cfg["latent"], cfg["noise"], cfg["r_max"], 1, nrows)
+    return orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, stream, 1, nrows,
+                        drift=cfg.get("drift", 0), k2=cfg.get("k2", 0), rho2=cfg.get("rho2", 0.9),
+                        scale2=cfg.get("scale2", 0.5))
+
+
+def cpu_other_rate(cfg, nrows, threads, sites=1):
+    """Oracle restatement of the config's update loop over rows 1..nrows."""
+    from oracle import pyoracle as orc
+    import numpy as np
+    orc.set_threads(threads)
+    ts = np.arange(1, nrows + 1)
+    if cfg["kind"] == "sw":
+        rows = oracle_stream(cfg, nrows)
+        s = orc.MlState(cfg["d"], cfg["window"], cfg["r_max"], cfg["eps"], 1, 1000)
+        t0 = time.perf_counter()
+        s.update_block(rows, ts)
+        return nrows / (time.perf_counter() - t0), nrows
+    if cfg["kind"] == "amm":
+        x, y = oracle_stream(cfg, nrows)
+        s = orc.CodState(cfg["dx"], cfg["dy"], cfg["eps"], cfg["eps"] * cfg["window"], cfg["window"], 1, 1000)
+        t0 = time.perf_counter()
+        s.update_block(x, y, ts)
+        return nrows / (time.perf_counter() - t0), nrows
+    streams = np.stack([oracle_stream(cfg, nrows, j) for j in range(sites)])
+    t0 = time.perf_counter()
+    orc.dist_run(streams, cfg["eps"], query_every=0, seed=1, probes=False)
+    return sites * nrows / (time.perf_counter() - t0), nrows
+
+
+def run_other(args, cfg, world, rank, local):
+    """C3 (MlState), C4 (distributed, one site per GPU), C5 (CodState)."""
+    import numpy as np
+    import torch
+    import paper_2601_02019_b200 as prod
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    S = args.rows_per_step or cfg["rows_per_step"]
+    steps, warm = args.steps, args.warmup
+    nrows = S * (steps + warm)
+    kind = cfg["kind"]
+    ts_all = np.arange(1, nrows + 1, dtype=np.int64)
+    if kind == "amm":
+        g = torch.Generator(device=dev).manual_seed(1)
+        W = torch.randn((cfg["latent"], cfg["dx"] + cfg["dy"]), generator=g, device=dev, dtype=torch.float64)
+        z = torch.randn((nrows, cfg["latent"]), generator=g, device=dev, dtype=torch.float64)
+        xy = z @ W + cfg["noise"] * torch.randn((nrows, cfg["dx"] + cfg["dy"]), generator=g, device=dev,
+                                                dtype=torch.float64)
+        x, y = xy[:, :cfg["dx"]].contiguous(), xy[:, cfg["dx"]:].contiguous()
+        for t in (x, y):  # squared norms log-uniform on (1, R]
+            u = torch.rand((nrows, 1), generator=g, device=dev, dtype=torch.float64)
+            t.mul_(torch.sqrt(cfg["r_max"] ** u / (t * t).sum(1, keepdim=True)))
+        x, y = x.cpu().numpy(), y.cpu().numpy()
+        state = prod.CodState(cfg["dx"], cfg["dy"], cfg["eps"], cfg["eps"] * cfg["window"], cfg["window"],
+                              seed=1, stream=1000, device=local)
+        upd = lambda sl: state.update_block(x[sl], y[sl], ts_all[sl])  # noqa: E731
+        unit_rows = 1
+    else:
+        rows = torch.empty((nrows, cfg["d"]), dtype=torch.float64, device=dev)
+        prod.gen_rows_device(rows, 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1,
+                             stream=rank, drift=cfg.get("drift", 0), k2=cfg.get("k2", 0),
+                             rho2=cfg.get("rho2", 0.9), scale2=cfg.get("scale2", 0.5), device=local)
+        torch.cuda.synchronize(dev)
+        if kind == "sw":
+            state = prod.MlState(cfg["d"], cfg["window"], cfg["r_max"], cfg["eps"], seed=1, stream=1000,
+                                 device=local)
+            upd = lambda sl: state.update_block(rows[sl], ts_all[sl])  # noqa: E731
+            unit_rows = 1
+        else:  # dist: sites j == rank (m = world)
+            from paper_2601_02019_b200.distributed import DistributedSketch
+            state = DistributedSketch(cfg["d"], cfg["eps"], world, seed=1, rank=rank, world=world,
+                                      group=group, device=local, use_nccl=world > 1)
+            upd = lambda sl: state.ingest({rank: rows[sl]}, sl.start + 1)  # noqa: E731
+            unit_rows = world
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for w in range(warm):
+        upd(slice(w * S, (w + 1) * S))
+    barrier()
+    l0 = prod.kernel_launches()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for k in range(warm, warm + steps):
+            upd(slice(k * S, (k + 1) * S))
+        barrier()
+        dt = time.perf_counter() - t0  # every update_block returns after its stream synchronized
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    value = unit_rows * S * steps / dt
+    extra = {}
+    if kind == "dist":
+        sk, _ = state.probe()  # NCCL merge (outside the timed region, like the reference's probes)
+        extra["probe_ok"] = bool(np.isfinite(sk).all())
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            rate, n_cpu = cpu_other_rate(cfg, args.cpu_rows or cfg["cpu_rows"], 1, sites=1)
+            cpu = {"value": rate, "unit": "rows/s" if kind != "dist" else "row-site updates/s", "cores": 1,
+                   "kind": "port", "sample": f"rows 1..{n_cpu} of {args.config.upper()} from an empty state"}
+        print(json.dumps({
+            "metric": "sketch update throughput", "value": value,
+            "unit": "row-site updates/s" if kind == "dist" else "rows/s", "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": dt * 1e3 / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "rows_per_step": S, "timed_rows": f"{warm * S + 1}..{nrows}",
+                       "parallelism": f"sites={world}" if kind == "dist" else "single",
+                       "timing": "host wall clock around blocking update_block calls (device work completes inside)"},
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(prod.kernel_launches() - l0),
+            "clocks": clk.summary(), **extra}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
@@ -168,6 +320,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, cfg, rank)
+        return
+    if cfg["kind"] != "attp":
+        run_other(args, cfg, world, rank, local)
         return
     import numpy as np
     import torch
