@@ -508,7 +508,10 @@ CodEngine::~CodEngine() {
     }
     cudaFree(im_->jobs_d);
     cudaFree(im_->status_d);
-    if (im_->st) cudaStreamDestroy(im_->st);
+    if (im_->st) {
+        eigh_forget(im_->st);
+        cudaStreamDestroy(im_->st);
+    }
     delete im_;
 }
 

@@ -24,7 +24,9 @@ struct Solver {
     int tmpw_n = 0;
 };
 std::mutex g_mu;
-std::unordered_map<int, Solver> g_solvers;  // per device
+// one solver (handle + workspace) per stream: sketches on different host
+// threads (MlState levels) must not share a workspace
+std::unordered_map<cudaStream_t, Solver> g_solvers;
 
 // reverse to descending order and fix signs (linalg.cpp:17-26, 66-75)
 __global__ void k_reverse_fix(int n, double* A, int lda, const double* wasc, double* wdesc) {
@@ -81,10 +83,12 @@ void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch, int6
         eigh_small(st, n, A, lda, w, batch, stride);
         return;
     }
-    int dev = 0;
-    AERO_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_mu);
-    Solver& s = g_solvers[dev];
+    Solver* sp;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        sp = &g_solvers[st];  // node-based map: the reference stays valid
+    }
+    Solver& s = *sp;
     if (!s.h) {
         if (cusolverDnCreate(&s.h) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate");
         AERO_CUDA(cudaMalloc(&s.info, sizeof(int)));
@@ -114,6 +118,18 @@ void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch, int6
         k_reverse_fix<<<n, 256, 0, st>>>(n, Ab, lda, s.tmpw, wb);
         AERO_LAUNCHED();
     }
+}
+
+void eigh_forget(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_solvers.find(st);
+    if (it == g_solvers.end()) return;
+    Solver& s = it->second;
+    if (s.work) cudaFree(s.work);
+    if (s.tmpw) cudaFree(s.tmpw);
+    if (s.info) cudaFree(s.info);
+    if (s.h) cusolverDnDestroy(s.h);
+    g_solvers.erase(it);
 }
 
 void eigh_release() {

@@ -362,6 +362,7 @@ Coordinator::~Coordinator() {
     cudaSetDevice(dev_);
     if (st_) {
         cudaStreamSynchronize(st_);
+        eigh_forget(st_);
         cudaStreamDestroy(st_);
     }
 }

@@ -76,6 +76,7 @@ constexpr int kSmallEigMax = 96;
 void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch = 1,
           int64_t stride = 0);
 void eigh_release();  // free cached solver handles/workspaces
+void eigh_forget(cudaStream_t st);  // free the solver cached for one stream
 
 // columns of V (n x ncol, ld) scaled: V[:, i] *= scale[i]
 void scale_columns(cudaStream_t st, int n, int ncol, double* V, int ld, const double* scale);

@@ -153,7 +153,10 @@ Sketch::~Sketch() {
     cudaFreeHost(clamp_h_);
     cudaFreeHost(nrm_h_);
     cudaFreeHost(bad_h_);
-    if (st_) cudaStreamDestroy(st_);
+    if (st_) {
+        eigh_forget(st_);
+        cudaStreamDestroy(st_);
+    }
 }
 
 void Sketch::set_theta(double th) {  // sketch.cpp:33-36
