@@ -295,10 +295,6 @@ __device__ void cta_eig_small(double* W, double* V, int k, double* cs) {
     __syncthreads();
 }
 
-__global__ void k_fill_cols_from_vec(double* dst, int ld, int rows, int col, const double* src) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < rows) dst[i + (int64_t)col * ld] = src[i];
-}
 }  // namespace
 
 struct CodSnap {

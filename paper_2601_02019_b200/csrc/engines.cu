@@ -15,7 +15,7 @@
 namespace aero_b200 {
 
 void shrink_device(cudaStream_t st, int d, int ell, double* B, double* w, double* out) {
-    eigh(st, d, B, d, w);
+    eigh(st, d, B, d, w, 1, 0, std::min(ell, d));
     shrink_rows(st, w, B, d, d, ell, out);
 }
 

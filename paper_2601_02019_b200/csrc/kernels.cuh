@@ -26,6 +26,11 @@ size_t product_workspace_doubles(int M, int N);
 bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
               const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
               size_t ws_doubles, int* splits_used = nullptr, bool defer_reduce = false);
+// Y = alpha op(A) op(B) + beta Y on the fast path (falls back to dgemm when
+// operand alignment rules the fast path out)
+void gemm_acc(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+              int lda, const double* B, int ldb, double beta, double* Y, int ldy, double* ws,
+              size_t ws_doubles);
 void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
                   int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles);
 
@@ -70,11 +75,13 @@ void iter_normalize_ws(cudaStream_t st, const IterJob* jobs, int njobs, int phas
 // symmetric eigendecomposition of `batch` n x n matrices (column-major, ld,
 // stride between matrices): eigenvalues descending, eigenvector columns
 // sign-fixed (largest-magnitude entry positive, linalg.cpp:17-26). A is
-// overwritten by V. Uses one-CTA Jacobi for n <= kSmallEigMax, cuSOLVER
-// syevd otherwise (round-1 stopgap).
-constexpr int kSmallEigMax = 96;
+// overwritten by V. One-CTA Jacobi for n <= kSmallEigMax, the tridiagonal
+// solver of syev.cu otherwise; nvec > 0 limits the eigenvectors to the top
+// nvec (columns nvec.. of A are then unspecified; all n eigenvalues returned).
+constexpr int kSmallEigMax = 32;
+constexpr int kBatchedJacobiMax = 96;
 void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch = 1,
-          int64_t stride = 0);
+          int64_t stride = 0, int nvec = 0);
 void eigh_release();  // free cached solver handles/workspaces
 void eigh_forget(cudaStream_t st);  // free the solver cached for one stream
 

@@ -39,7 +39,8 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(PNT, 2)
     k_product(int M, int N, int K, int kchunk, const double* __restrict__ A, int lda,
               const double* __restrict__ B, int ldb, double* __restrict__ out, int ldo,
-              int64_t split_stride, const int* __restrict__ colmask, int direct) {
+              int64_t split_stride, const int* __restrict__ colmask, int direct, double alpha,
+              double beta) {
     extern __shared__ __align__(16) double smd[];
     double* sa = smd;
     double* sb = smd + PST * A_TILE;
@@ -142,7 +143,9 @@ __global__ void __launch_bounds__(PNT, 2)
         for (int i = 0; i < 8; ++i) {
             const int gm = bm + tr + 16 * i;
             if (gm >= M) continue;
-            o[gm + (int64_t)gn * ldo] = (gm < lim) ? acc[i][j] : 0.0;
+            double* dst = o + gm + (int64_t)gn * ldo;
+            if (!direct || (alpha == 1.0 && beta == 0.0)) *dst = (gm < lim) ? acc[i][j] : 0.0;
+            else *dst = (gm < lim) ? fma(alpha, acc[i][j], beta == 0.0 ? 0.0 : beta * *dst) : 0.0;
         }
     }
 }
@@ -150,20 +153,22 @@ __global__ void __launch_bounds__(PNT, 2)
 // fixed-order sum of the split-K partials + row mask
 __global__ void k_product_reduce(int M, int N, int splits, const double* __restrict__ ws,
                                  int64_t split_stride, double* __restrict__ Y, int ldy,
-                                 const int* __restrict__ colmask) {
+                                 const int* __restrict__ colmask, double alpha, double beta) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (int64_t)M * N) return;
     const int i = (int)(e % M), j = (int)(e / M);
     double v = 0.0;
     for (int z = 0; z < splits; ++z) v += ws[z * split_stride + e];
+    double* dst = Y + i + (int64_t)j * ldy;
+    if (alpha != 1.0 || beta != 0.0) v = fma(alpha, v, beta == 0.0 ? 0.0 : beta * *dst);
     if (colmask && i >= colmask[j]) v = 0.0;
-    Y[i + (int64_t)j * ldy] = v;
+    *dst = v;
 }
 
 template <bool TA, bool TB>
 void launch(cudaStream_t st, dim3 grid, int M, int N, int K, int kchunk, const double* A, int lda,
             const double* B, int ldb, double* out, int ldo, int64_t sstride, const int* colmask,
-            int direct) {
+            int direct, double alpha, double beta) {
     static bool attr = false;
     if (!attr) {
         AERO_CUDA(cudaFuncSetAttribute(k_product<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -171,16 +176,17 @@ void launch(cudaStream_t st, dim3 grid, int M, int N, int K, int kchunk, const d
         attr = true;
     }
     k_product<TA, TB><<<grid, PNT, PROD_SMEM, st>>>(M, N, K, kchunk, A, lda, B, ldb, out, ldo,
-                                                    sstride, colmask, direct);
+                                                    sstride, colmask, direct, alpha, beta);
     AERO_LAUNCHED();
 }
 }  // namespace
 
 size_t product_workspace_doubles(int M, int N) { return (size_t)8 * M * N; }
 
-bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
-              const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
-              size_t ws_doubles, int* splits_used, bool defer_reduce) {
+namespace {
+bool gemm_core(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+               int lda, const double* B, int ldb, double beta, double* Y, int ldy, const int* colmask,
+               double* ws, size_t ws_doubles, int* splits_used, bool defer_reduce) {
     if (M <= 0 || N <= 0) return true;
     // 16-byte cp.async needs even leading dimensions and aligned bases
     if ((lda & 1) || (ldb & 1) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15)) return false;
@@ -195,18 +201,34 @@ bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const doub
     double* o = splits == 1 ? Y : ws;
     const int ldo = splits == 1 ? ldy : M;
     const int direct = splits == 1;
-    if (!ta && !tb) launch<false, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
-    else if (ta && !tb) launch<true, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
-    else if (!ta && tb) launch<false, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
-    else launch<true, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct);
+    if (!ta && !tb) launch<false, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct, alpha, beta);
+    else if (ta && !tb) launch<true, false>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct, alpha, beta);
+    else if (!ta && tb) launch<false, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct, alpha, beta);
+    else launch<true, true>(st, grid, M, N, K, kchunk, A, lda, B, ldb, o, ldo, sstride, colmask, direct, alpha, beta);
     if (splits_used) *splits_used = splits;
     if (splits > 1 && !defer_reduce) {
         const int64_t tot = (int64_t)M * N;
         k_product_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, N, splits, ws, sstride, Y,
-                                                                        ldy, colmask);
+                                                                        ldy, colmask, alpha, beta);
         AERO_LAUNCHED();
     }
     return true;
+}
+}  // namespace
+
+bool gemm_big(cudaStream_t st, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+              const double* B, int ldb, double* Y, int ldy, const int* colmask, double* ws,
+              size_t ws_doubles, int* splits_used, bool defer_reduce) {
+    return gemm_core(st, ta, tb, M, N, K, 1.0, A, lda, B, ldb, 0.0, Y, ldy, colmask, ws, ws_doubles,
+                     splits_used, defer_reduce);
+}
+
+void gemm_acc(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+              int lda, const double* B, int ldb, double beta, double* Y, int ldy, double* ws,
+              size_t ws_doubles) {
+    if (!gemm_core(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, Y, ldy, nullptr, ws, ws_doubles,
+                   nullptr, false))
+        dgemm(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, Y, ldy);
 }
 
 void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,

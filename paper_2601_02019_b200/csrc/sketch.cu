@@ -226,7 +226,7 @@ void Sketch::reduce() {
     ew_.alloc(n);
     fw_.alloc(n);
     copy_matrix(st_, n, n, G_.p, cap_, E_.p, n);
-    eigh(st_, n, E_.p, n, ew_.p);
+    eigh(st_, n, E_.p, n, ew_.p, 1, 0, keep);  // only the kept directions
     fd_weights(st_, ew_.p, n, ell_, keep, fw_.p);
     scale_columns(st_, n, keep, E_.p, n, fw_.p);
     if (!gemm_big(st_, false, false, d_, keep, n, C_.p, d_, E_.p, n, C2_.p, d_, nullptr, ws_.p, ws_.n))
@@ -761,7 +761,7 @@ void Sketch::query(int64_t lb, int64_t ub, double* out_host) {
     const double* B = query_gram_device(lb, ub);
     copy_matrix(st_, d_, d_, B, d_, Wq_.p, d_);
     double* w = Wq_.p + (size_t)d_ * d_;
-    eigh(st_, d_, Wq_.p, d_, w);
+    eigh(st_, d_, Wq_.p, d_, w, 1, 0, std::min(ell_, d_));
     qy_.alloc((size_t)ell_ * d_);
     shrink_rows(st_, w, Wq_.p, d_, d_, ell_, qy_.p);
     AERO_CUDA(cudaMemcpyAsync(out_host, qy_.p, sizeof(double) * ell_ * d_, cudaMemcpyDeviceToHost, st_));

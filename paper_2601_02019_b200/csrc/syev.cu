@@ -1,0 +1,896 @@
+// Symmetric eigensolver for n > kSmallEigMax (the FD reduce at C2: n = 2ell =
+// 2048; C3/C5: 256; C4: 512; query shrink: n = d). Replaces the reference's
+// Eigen SelfAdjointEigenSolver / BDCSVD (linalg.cpp:48-76) on the device:
+//
+//  1. k_sytrd   -- Householder tridiagonalization Q^T A Q = T in ONE persistent
+//                  cooperative kernel: LAPACK-style blocked panels (dlatrd
+//                  recurrence, 32 columns) with a grid barrier per phase; the
+//                  panel symv reads whole columns of the symmetric trailing
+//                  block (coalesced, L2-resident), the syr2k trailing update
+//                  runs as 64x64 register tiles over the lower triangle and is
+//                  mirrored, so both triangles stay current.
+//  2. k_bisect  -- all eigenvalues of T by 33-way multisection (one warp per
+//                  eigenvalue, Sturm counts per lane).
+//  3. k_twisted -- eigenvectors of T for the top `nvec` eigenvalues from a
+//                  twisted LDL^T/UDU^T factorization (one thread per vector,
+//                  row-interleaved scratch so the qd sweeps coalesce), then
+//                  modified Gram-Schmidt inside tight clusters.
+//  4. back-transform Z = Q Y with compact-WY blocks of 128 reflectors
+//                  (T factor per block, three fp64 GEMMs on the product engine).
+// Output convention of eigh(): eigenvalues descending, eigenvector columns
+// sign-fixed so the largest-magnitude entry is positive (linalg.cpp:17-26).
+#include <cooperative_groups.h>
+#include <cuda/atomic>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cfloat>
+#include <mutex>
+#include <unordered_map>
+
+#include "aero_common.cuh"
+#include "kernels.cuh"
+#include "sketch.hpp"  // DeviceBuf
+
+namespace aero_b200 {
+
+namespace {
+constexpr int TRD_NB = 32;        // panel width (reflectors per panel)
+constexpr int TRD_THREADS = 256;  // 8 warps
+constexpr int TRD_TILE = 64;      // trailing-update tile
+constexpr int SLOTW = 4;          // doubles per CTA partial slot
+constexpr int BT_NB = 128;        // reflectors per back-transform block
+
+// monotone arrival counter (zeroed before the launch): release-add, acquire-spin
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch, unsigned nblocks) {
+    __syncthreads();
+    epoch += nblocks;
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> c(*ctr);
+        c.fetch_add(1u, cuda::memory_order_release);
+        while (c.load(cuda::memory_order_acquire) < epoch) {
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// fixed-order block sum (deterministic for a fixed block size)
+__device__ double block_sum_d(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum_d(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    return s;
+}
+
+// sum of slot field f over all CTAs in a fixed order (every thread gets it)
+__device__ double slots_sum(const double* slots, int f, int G, double* red) {
+    double v = 0.0;
+    if (threadIdx.x < 32) {
+        for (int c = threadIdx.x; c < G; c += 32) v += __ldcg(slots + c * SLOTW + f);
+        v = warp_sum_d(v);
+        if (threadIdx.x == 0) red[32] = v;
+    }
+    __syncthreads();
+    const double s = red[32];
+    __syncthreads();
+    return s;
+}
+
+constexpr int TRD_NW = TRD_THREADS / 32;
+
+struct TrdArgs {
+    int n, lda;
+    double* A;  // n x n symmetric, both triangles current (overwritten)
+    double* V;  // n x n explicit reflectors (ld n, zero-initialized): column j = v_j, v_j[j+1] = 1
+    double* W;  // n x TRD_NB panel W (ld n)
+    double *d, *e, *tau;
+    double *ybuf, *wpre, *y0, *slots, *dots;
+    unsigned* bar;
+    unsigned long long* prof;  // optional per-phase ns accumulators (CTA 0, dev instrumentation)
+};
+
+
+// LAPACK dsytrd (lower) with the dlatrd panel recurrence and dlarfg reflectors,
+// restated for a persistent grid with TWO grid barriers per column: every CTA
+// rebuilds the next column (and its reflector) redundantly in shared memory
+// from the published partial column y0, so no barrier is spent on the norm,
+// and every row-local input is prefetched before the barrier that precedes
+// its use (the kernel is L2-latency bound; each phase is one load round).
+//  per column j (panel i0, jj = j - i0):
+//   R   (all CTAs) beta, tau, v from the column in sx           -> sv[cur]
+//   B   y = A(j+1:, j+1:) v (warp per column, 16 B loads), dots V^T v, W^T v;
+//       own rows: V(r, k), W(r, k) into registers, panel part of y0
+//   -- barrier --
+//   C   own rows: w = tau (y - W V^T v - V W^T v); partial w.v; y0
+//   -- barrier --
+//   A'  alpha2 = -tau/2 w.v; W(:, jj) = w + alpha2 v; x' = y0 - v (w_{j+1} + 2 alpha2)
+// W(:, jj) reaches global memory without a barrier before the next column,
+// so that column evaluates it as wpre + alpha2 v_prev wherever it needs it.
+template <bool VEC>
+__global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int n = a.n, G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int gw = cta * TRD_NW + warp, GW = G * TRD_NW;
+    const int gwi = warp * G + cta;          // CTA-interleaved warp index (row phases)
+    const int sub = lane & 7, grp = lane >> 3;  // 8 lanes per row, 4 rows per warp
+    const int lda = a.lda;
+    const int npad = (n + 3) & ~1;
+    double* red = sm;                          // 64
+    double* sx = sm + 64;                      // npad: column being reduced, sx[r - j]
+    double* svb = sx + npad;                   // 2 x npad: reflectors (ping-pong), sv[c - c0]
+    double* srow = svb + 2 * npad;             // 2 * TRD_NB: W(j+1, k) | V(j+1, i0 + k)
+    double* sdot = srow + 2 * TRD_NB;          // 2 * TRD_NB: V^T v | W^T v
+    double* tl = sdot + 2 * TRD_NB;            // 4 * TRD_TILE * TRD_NB
+    double* A = a.A;
+    double* V = a.V;
+    double* W = a.W;
+    unsigned epoch = 0;
+    int cur = 0;
+    double a2prev = 0.0;  // alpha2 of the previous column (same panel)
+    int c0prev = 0;
+    double s2p = 0.0;     // this thread's part of ||x[2:]||^2 for the column in sx
+    unsigned long long tp = clock64();
+#define TRD_MARK(i)                                                   \
+    if (a.prof && cta == 0 && tid == 0) {                             \
+        const unsigned long long t_ = clock64();                      \
+        a.prof[i] += t_ - tp;                                         \
+        tp = t_;                                                      \
+    }
+
+    for (int r = tid; r < n; r += TRD_THREADS) {  // column 0
+        const double x = A[r];
+        sx[r] = x;
+        if (r >= 2) s2p += x * x;
+    }
+
+    for (int i0 = 0; i0 < n - 1; i0 += TRD_NB) {
+        const int jb = min(TRD_NB, n - 1 - i0);
+        for (int jj = 0; jj < jb; ++jj) {
+            const int j = i0 + jj;
+            const int m = n - j - 1;  // reflector length: rows j+1 .. n-1
+            const bool nxt = jj + 1 < jb;
+            // ---- R: reflector (dlarfg) from sx, identical in every CTA
+            const double s2 = block_sum_d(s2p, red);
+            const double alpha = sx[1];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (s2 > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            const int c0 = (j + 1) & ~1;
+            double* sv = svb + cur * npad;
+            const double* svo = svb + (cur ^ 1) * npad;  // previous reflector (index c - c0prev)
+            for (int c = c0 + tid; c < n + 1; c += TRD_THREADS) {
+                const int i = c - (j + 1);
+                sv[c - c0] = (c >= n || i < 0) ? 0.0 : (i == 0 ? 1.0 : sx[i + 1] * scal);
+            }
+            if (nxt && tid < jj) {  // row j+1 of the panel (W(j+1, jj-1) not yet in W)
+                srow[tid] = (tid == jj - 1) ? __ldcg(a.wpre + j + 1) + a2prev * svo[j + 1 - c0prev]
+                                            : __ldcg(W + j + 1 + (int64_t)tid * n);
+                srow[TRD_NB + tid] = __ldcg(V + j + 1 + (int64_t)(i0 + tid) * n);
+            }
+            if (cta == 0 && tid == 0) {
+                a.d[j] = sx[0];
+                a.e[j] = beta;
+                a.tau[j] = tau;
+            }
+            __syncthreads();
+            if (cta == 0)
+                for (int i = tid; i < m; i += TRD_THREADS) V[j + 1 + i + (int64_t)j * n] = sv[j + 1 + i - c0];
+            TRD_MARK(0);
+
+            // ---- B: symv on the panel-start trailing block + panel dots
+            if (tau != 0.0) {
+                const int len = n - c0;
+                for (int r = j + 1 + gw; r < n; r += GW) {
+                    const double* col = A + (int64_t)r * lda + c0;
+                    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+                    if (VEC) {  // 8 x 16 B loads in flight per lane
+                        const double2* c2 = reinterpret_cast<const double2*>(col);
+                        const double2* v2 = reinterpret_cast<const double2*>(sv);
+                        const int np = len >> 1;
+                        int p = lane;
+                        for (; p + 224 < np; p += 256) {
+                            double2 x[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) x[u] = __ldcg(c2 + p + 32 * u);
+#pragma unroll
+                            for (int u = 0; u < 8; u += 4) {
+                                const double2 y0 = v2[p + 32 * u], y1 = v2[p + 32 * (u + 1)];
+                                const double2 y2 = v2[p + 32 * (u + 2)], y3 = v2[p + 32 * (u + 3)];
+                                acc0 = fma(x[u].x, y0.x, fma(x[u].y, y0.y, acc0));
+                                acc1 = fma(x[u + 1].x, y1.x, fma(x[u + 1].y, y1.y, acc1));
+                                acc2 = fma(x[u + 2].x, y2.x, fma(x[u + 2].y, y2.y, acc2));
+                                acc3 = fma(x[u + 3].x, y3.x, fma(x[u + 3].y, y3.y, acc3));
+                            }
+                        }
+                        double2 x[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            x[u] = (p + 32 * u < np) ? __ldcg(c2 + p + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (p + 32 * u < np) {
+                                const double2 y = v2[p + 32 * u];
+                                acc0 = fma(x[u].x, y.x, fma(x[u].y, y.y, acc0));
+                            }
+                        if ((len & 1) && lane == 0) acc1 = fma(col[len - 1], sv[len - 1], acc1);
+                    } else {
+                        int c = lane;
+                        for (; c + 96 < len; c += 128) {
+                            acc0 = fma(col[c], sv[c], acc0);
+                            acc1 = fma(col[c + 32], sv[c + 32], acc1);
+                            acc2 = fma(col[c + 64], sv[c + 64], acc2);
+                            acc3 = fma(col[c + 96], sv[c + 96], acc3);
+                        }
+                        for (; c < len; c += 32) acc0 = fma(col[c], sv[c], acc0);
+                    }
+                    const double acc = warp_sum_d((acc0 + acc1) + (acc2 + acc3));
+                    if (lane == 0) a.ybuf[r] = acc;
+                }
+                for (int q = GW - 1 - gw; q < 2 * jj; q += GW) {
+                    double acc0 = 0.0, acc1 = 0.0;
+                    if (q < jj) {  // V(:, i0+q)^T v
+                        const double* col = V + (int64_t)(i0 + q) * n;
+                        for (int c = j + 1 + lane; c < n; c += 64) {
+                            acc0 = fma(__ldcg(col + c), sv[c - c0], acc0);
+                            if (c + 32 < n) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
+                        }
+                    } else if (q - jj < jj - 1) {  // W(:, k)^T v, final columns
+                        const double* col = W + (int64_t)(q - jj) * n;
+                        for (int c = j + 1 + lane; c < n; c += 64) {
+                            acc0 = fma(__ldcg(col + c), sv[c - c0], acc0);
+                            if (c + 32 < n) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
+                        }
+                    } else {  // W(:, jj-1) = wpre + alpha2 v_prev
+                        for (int c = j + 1 + lane; c < n; c += 32)
+                            acc0 = fma(__ldcg(a.wpre + c) + a2prev * svo[c - c0prev], sv[c - c0], acc0);
+                    }
+                    const double acc = warp_sum_d(acc0 + acc1);
+                    if (lane == 0) a.dots[q] = acc;
+                }
+            }
+            // own-row panel values (final before this column) and the panel part of y0
+            const int r = j + 1 + 4 * gwi + grp;
+            const bool valid = r < n;
+            double pv[4], pw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = sub + 8 * u;
+                pv[u] = 0.0;
+                pw[u] = 0.0;
+                if (valid && k < jj) {
+                    pv[u] = __ldcg(V + r + (int64_t)(i0 + k) * n);
+                    pw[u] = (k == jj - 1) ? __ldcg(a.wpre + r) + a2prev * svo[r - c0prev]
+                                          : __ldcg(W + r + (int64_t)k * n);
+                }
+            }
+            const double anext = (valid && sub == 0 && nxt) ? __ldcg(A + r + (int64_t)(j + 1) * lda) : 0.0;
+            double ypart = 0.0;
+            if (nxt) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = sub + 8 * u;
+                    if (k < jj) ypart = fma(pv[u], srow[k], fma(pw[u], srow[TRD_NB + k], ypart));
+                }
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) ypart += __shfl_xor_sync(0xffffffffu, ypart, o);
+            }
+            TRD_MARK(1);
+            grid_sync(a.bar, epoch, G);
+            TRD_MARK(2);
+
+            // ---- C: own rows
+            if (tid < 2 * jj) sdot[tid] = (tau != 0.0) ? __ldcg(a.dots + tid) : 0.0;
+            const double yb = (valid && sub == 0 && tau != 0.0) ? __ldcg(a.ybuf + r) : 0.0;
+            __syncthreads();
+            double t = 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = sub + 8 * u;
+                if (k < jj) t = fma(pw[u], sdot[k], fma(pv[u], sdot[jj + k], t));
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            double wv = 0.0, wr = 0.0;
+            if (valid && sub == 0) {
+                wr = (tau != 0.0) ? tau * (yb - t) : 0.0;
+                a.wpre[r] = wr;
+                wv = wr * sv[r - c0];
+                if (nxt) a.y0[r] = anext - ypart - wr;
+            }
+            wv = block_sum_d(wv, red);
+            if (tid == 0) a.slots[cta * SLOTW + 1] = wv;
+            TRD_MARK(3);
+            grid_sync(a.bar, epoch, G);
+            TRD_MARK(4);
+
+            // ---- A': finish W(:, jj) (own rows), next column into sx
+            double yv[16];
+            const double wj1 = nxt ? __ldcg(a.wpre + j + 1) : 0.0;
+            if (nxt) {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int rr = j + 1 + tid + u * TRD_THREADS;
+                    yv[u] = (rr < n) ? __ldcg(a.y0 + rr) : 0.0;
+                }
+            }
+            const double a2 = -0.5 * tau * slots_sum(a.slots, 1, G, red);
+            if (valid && sub == 0) W[r + (int64_t)jj * n] = wr + a2 * sv[r - c0];
+            if (nxt) {
+                const double coef = wj1 + 2.0 * a2;
+                s2p = 0.0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int rr = j + 1 + tid + u * TRD_THREADS;
+                    if (rr < n) {
+                        const double x = yv[u] - sv[rr - c0] * coef;
+                        sx[rr - j - 1] = x;
+                        if (rr >= j + 3) s2p += x * x;
+                    }
+                }
+                a2prev = a2;
+                c0prev = c0;
+            } else {
+                a2prev = 0.0;
+            }
+            cur ^= 1;
+            TRD_MARK(5);
+        }
+        grid_sync(a.bar, epoch, G);
+        TRD_MARK(6);
+        const int t0 = i0 + jb, mt = n - t0;
+        if (mt > 0) {
+            const int nt = (mt + TRD_TILE - 1) / TRD_TILE;
+            const int ntiles = nt * (nt + 1) / 2;
+            double* sVr = tl;                       // [k][64] rows R of V
+            double* sWr = sVr + TRD_NB * TRD_TILE;  // rows R of W
+            double* sVc = sWr + TRD_NB * TRD_TILE;  // rows C of V
+            double* sWc = sVc + TRD_NB * TRD_TILE;  // rows C of W
+            const int tr = tid & 15, tc = tid >> 4;  // 16 x 16 threads, 4 x 4 each
+            for (int t = cta; t < ntiles; t += G) {
+                int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);  // t = bi(bi+1)/2 + bj
+                while (bi * (bi + 1) / 2 > t) --bi;
+                while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+                const int bj = t - bi * (bi + 1) / 2;
+                const int R0 = t0 + bi * TRD_TILE, C0 = t0 + bj * TRD_TILE;
+                __syncthreads();
+                for (int idx = tid; idx < TRD_NB * TRD_TILE; idx += TRD_THREADS) {
+                    const int k = idx / TRD_TILE, i = idx % TRD_TILE;
+                    const bool kin = k < jb;
+                    const int rr = R0 + i, c = C0 + i;
+                    sVr[idx] = (kin && rr < n) ? __ldcg(V + rr + (int64_t)(i0 + k) * n) : 0.0;
+                    sWr[idx] = (kin && rr < n) ? __ldcg(W + rr + (int64_t)k * n) : 0.0;
+                    sVc[idx] = (kin && c < n) ? __ldcg(V + c + (int64_t)(i0 + k) * n) : 0.0;
+                    sWc[idx] = (kin && c < n) ? __ldcg(W + c + (int64_t)k * n) : 0.0;
+                }
+                __syncthreads();
+                double acc[4][4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+                for (int k = 0; k < jb; ++k) {
+                    double vr[4], wr4[4], vc[4], wc[4];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        vr[p] = sVr[k * TRD_TILE + tr + 16 * p];
+                        wr4[p] = sWr[k * TRD_TILE + tr + 16 * p];
+                        vc[p] = sVc[k * TRD_TILE + tc + 16 * p];
+                        wc[p] = sWc[k * TRD_TILE + tc + 16 * p];
+                    }
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[p][q] = fma(vr[p], wc[q], fma(wr4[p], vc[q], acc[p][q]));
+                }
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const int rr = R0 + tr + 16 * p;
+                    if (rr >= n) continue;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = C0 + tc + 16 * q;
+                        if (c >= n) continue;
+                        A[rr + (int64_t)c * lda] -= acc[p][q];
+                        if (bi != bj) A[c + (int64_t)rr * lda] -= acc[p][q];
+                    }
+                }
+            }
+        }
+        TRD_MARK(7);
+        grid_sync(a.bar, epoch, G);
+        s2p = 0.0;
+        for (int rr = t0 + tid; rr < n; rr += TRD_THREADS) {
+            const double x = __ldcg(A + rr + (int64_t)t0 * lda);
+            sx[rr - t0] = x;
+            if (rr >= t0 + 2) s2p += x * x;
+        }
+        __syncthreads();
+        TRD_MARK(8);
+    }
+    if (cta == 0 && tid == 0) a.d[n - 1] = sx[0];
+#undef TRD_MARK
+}
+
+// Small n (<= kSytrdSmall): unblocked dsytd2 by ONE CTA with the whole matrix
+// in shared memory (no grid barriers). Same outputs as k_sytrd.
+constexpr int kSytrdSmall = 128;
+__global__ void __launch_bounds__(512, 1) k_sytrd_small(int n, const double* __restrict__ Ain, int lda,
+                                                        double* __restrict__ V, double* __restrict__ d,
+                                                        double* __restrict__ e, double* __restrict__ tau) {
+    extern __shared__ __align__(16) double sa[];  // n*n matrix (ld n), v[n], w[n], red[64]
+    double* sv = sa + n * n;
+    double* sw = sv + n;
+    double* red = sw + n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int idx = tid; idx < n * n; idx += nt) sa[idx] = Ain[idx % n + (int64_t)(idx / n) * lda];
+    __syncthreads();
+    for (int j = 0; j < n - 1; ++j) {
+        const int m = n - j - 1;  // rows j+1 .. n-1
+        double s2 = 0.0;
+        for (int i = j + 2 + tid; i < n; i += nt) s2 += sa[i + j * n] * sa[i + j * n];
+        s2 = block_sum_d(s2, red);
+        const double alpha = sa[j + 1 + j * n];
+        double tj = 0.0, beta = alpha, scal = 0.0;
+        if (s2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+            tj = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int i = tid; i < m; i += nt) {
+            const double v = (i == 0) ? 1.0 : sa[j + 1 + i + j * n] * scal;
+            sv[i] = v;
+            V[j + 1 + i + (int64_t)j * n] = v;
+        }
+        if (tid == 0) {
+            d[j] = sa[j + j * n];
+            e[j] = beta;
+            tau[j] = tj;
+        }
+        __syncthreads();
+        if (tj == 0.0) continue;
+        // p = tau A22 v  (A22 = sa[j+1:, j+1:]; consecutive threads take consecutive rows)
+        for (int r = tid; r < m; r += nt) {
+            const double* row = sa + (j + 1 + r) + (j + 1) * n;
+            double acc = 0.0;
+            for (int c = 0; c < m; ++c) acc = fma(row[c * n], sv[c], acc);
+            sw[r] = tj * acc;
+        }
+        __syncthreads();
+        double pv = 0.0;
+        for (int i = tid; i < m; i += nt) pv += sw[i] * sv[i];
+        pv = block_sum_d(pv, red);
+        const double K = -0.5 * tj * pv;
+        for (int i = tid; i < m; i += nt) sw[i] += K * sv[i];
+        __syncthreads();
+        // A22 -= v w^T + w v^T
+        for (int idx = tid; idx < m * m; idx += nt) {
+            const int r = idx % m, c = idx / m;
+            sa[(j + 1 + r) + (j + 1 + c) * n] -= sv[r] * sw[c] + sw[r] * sv[c];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) d[n - 1] = sa[(n - 1) + (n - 1) * n];
+}
+
+// Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x
+__device__ __forceinline__ int sturm_count(int n, const double* d, const double* e2, double x,
+                                           double pivmin) {
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        q = d[i] - x - e2[i - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
+// one warp per eigenvalue index k (ascending, k >= k_lo): 33-way multisection
+// of the Gershgorin interval; d and e^2 staged in shared memory
+__global__ void k_bisect(int n, int k_lo, const double* __restrict__ d, const double* __restrict__ e2,
+                         const double* __restrict__ bounds, double* __restrict__ lam_asc) {
+    extern __shared__ double sde[];
+    double* sd = sde;
+    double* se = sde + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sd[i] = d[i];
+        se[i] = (i < n - 1) ? e2[i] : 0.0;
+    }
+    __syncthreads();
+    const int k = k_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= n) return;
+    const double pivmin = bounds[2];
+    double lo = bounds[0], hi = bounds[1];
+    for (int round = 0; round < 64; ++round) {
+        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
+        if (hi - lo <= tol) break;
+        const double h = (hi - lo) / 33.0;
+        const double x = fmin(lo + h * (lane + 1), hi);
+        const int c = sturm_count(n, sd, se, x, pivmin);
+        const unsigned above = __ballot_sync(0xffffffffu, c > k);
+        double nlo = lo, nhi = hi;
+        if (above) {
+            const int f = __ffs(above) - 1;
+            nhi = __shfl_sync(0xffffffffu, x, f);
+            const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+            if (f > 0) nlo = xp;
+        } else {
+            nlo = __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (nlo == lo && nhi == hi) break;  // interval can no longer be split
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) lam_asc[k] = 0.5 * (lo + hi);
+}
+
+// Gershgorin interval, pivmin, ||T||, e^2 (one CTA)
+__global__ void k_tri_prep(int n, const double* __restrict__ d, const double* __restrict__ e,
+                           double* __restrict__ e2, double* __restrict__ bounds) {
+    __shared__ double smin[32], smax[32], se[32];
+    double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double el = (i > 0) ? fabs(e[i - 1]) : 0.0;
+        const double er = (i < n - 1) ? fabs(e[i]) : 0.0;
+        lo = fmin(lo, d[i] - el - er);
+        hi = fmax(hi, d[i] + el + er);
+        if (i < n - 1) {
+            e2[i] = e[i] * e[i];
+            emax = fmax(emax, e2[i]);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        smin[wid] = lo;
+        smax[wid] = hi;
+        se[wid] = emax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) {
+            lo = fmin(lo, smin[w]);
+            hi = fmax(hi, smax[w]);
+            emax = fmax(emax, se[w]);
+        }
+        const double tnorm = fmax(fabs(lo), fabs(hi));
+        const double pivmin = DBL_MIN * fmax(1.0, emax);
+        const double pad = 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
+        bounds[0] = lo - pad;
+        bounds[1] = hi + pad;
+        bounds[2] = pivmin;
+        bounds[3] = tnorm;
+    }
+}
+
+// eigenvector of T for lam (descending index q) by a twisted factorization.
+// Scratch Dp and output Z are row-interleaved: element i of vector q at
+// [i * nvec + q] so consecutive threads touch consecutive addresses.
+__global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const double* __restrict__ e,
+                          const double* __restrict__ lam_asc, const double* __restrict__ bounds,
+                          double* __restrict__ Dp, double* __restrict__ Z) {
+    extern __shared__ double sde[];
+    double* sd = sde;
+    double* se = sde + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sd[i] = d[i];
+        se[i] = (i < n - 1) ? e[i] : 0.0;
+    }
+    __syncthreads();
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nvec) return;
+    const double lam = lam_asc[n - 1 - q];
+    const double pivmin = bounds[2];
+    auto safe = [&](double x) { return (fabs(x) < pivmin) ? -pivmin : x; };
+    // top-down stationary qd: D+(i)
+    double dp = safe(sd[0] - lam);
+    Dp[q] = dp;
+    for (int i = 0; i < n - 1; ++i) {
+        dp = safe(sd[i + 1] - lam - se[i] * (se[i] / dp));
+        Dp[(int64_t)(i + 1) * nvec + q] = dp;
+    }
+    // bottom-up: D-(i) into Z, twist index by min |gamma|
+    double dm = safe(sd[n - 1] - lam);
+    Z[(int64_t)(n - 1) * nvec + q] = dm;
+    int r = n - 1;
+    double best = fabs(dp);  // gamma_{n-1} = D+(n-1)
+#pragma unroll 4
+    for (int i = n - 2; i >= 0; --i) {
+        const double dpi = Dp[(int64_t)i * nvec + q];
+        dm = safe(sd[i] - lam - se[i] * (se[i] / dm));
+        Z[(int64_t)i * nvec + q] = dm;
+        const double g = dpi + dm - (sd[i] - lam);
+        if (fabs(g) < best) {
+            best = fabs(g);
+            r = i;
+        }
+    }
+    // solve outward from r
+    double nrm2 = 1.0, z = 1.0;
+#pragma unroll 4
+    for (int i = r; i < n - 1; ++i) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
+        const double dmn = Z[(int64_t)(i + 1) * nvec + q];
+        z = -(se[i] / dmn) * z;
+        Z[(int64_t)(i + 1) * nvec + q] = z;
+        nrm2 += z * z;
+    }
+    Z[(int64_t)r * nvec + q] = 1.0;
+    z = 1.0;
+#pragma unroll 4
+    for (int i = r - 1; i >= 0; --i) {  // z_i = -(e_i / D+(i)) z_{i+1}
+        z = -(se[i] / Dp[(int64_t)i * nvec + q]) * z;
+        Z[(int64_t)i * nvec + q] = z;
+        nrm2 += z * z;
+    }
+    const double s = 1.0 / sqrt(nrm2);
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) Z[(int64_t)i * nvec + q] *= s;
+}
+
+// modified Gram-Schmidt inside clusters of close eigenvalues (one warp per
+// cluster leader; clusters longer than kMaxCluster are left as computed)
+constexpr int kMaxCluster = 128;
+__global__ void k_cluster_mgs(int n, int nvec, const double* __restrict__ lam_asc,
+                              const double* __restrict__ bounds, double* __restrict__ Z) {
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nvec) return;
+    const double thr = 1e-7 * bounds[3] + bounds[2];
+    auto lam = [&](int i) { return lam_asc[n - 1 - i]; };  // descending
+    if (q > 0 && lam(q - 1) - lam(q) <= thr) return;        // not a leader
+    int end = q + 1;
+    while (end < nvec && lam(end - 1) - lam(end) <= thr && end - q < kMaxCluster) ++end;
+    if (end - q < 2) return;
+    for (int i = q; i < end; ++i) {
+        for (int p = q; p < i; ++p) {
+            double dot = 0.0;
+            for (int t = lane; t < n; t += 32) dot += Z[(int64_t)t * nvec + p] * Z[(int64_t)t * nvec + i];
+            dot = warp_sum_d(dot);
+            for (int t = lane; t < n; t += 32) Z[(int64_t)t * nvec + i] -= dot * Z[(int64_t)t * nvec + p];
+        }
+        double nr = 0.0;
+        for (int t = lane; t < n; t += 32) nr += Z[(int64_t)t * nvec + i] * Z[(int64_t)t * nvec + i];
+        nr = warp_sum_d(nr);
+        const double s = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+        for (int t = lane; t < n; t += 32) Z[(int64_t)t * nvec + i] *= s;
+    }
+}
+
+// Y (n x nvec column-major) = Z^T view (Z row-interleaved n x nvec)
+__global__ void k_interleaved_to_cols(int n, int nvec, const double* __restrict__ Z, double* __restrict__ Y,
+                                      int ldy) {
+    __shared__ double tile[32][33];
+    const int i0 = blockIdx.x * 32, q0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, q = q0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < n && q < nvec) ? Z[(int64_t)i * nvec + q] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int q = q0 + r, i = i0 + threadIdx.x;
+        if (q < nvec && i < n) Y[i + (int64_t)q * ldy] = tile[threadIdx.x][r];
+    }
+}
+
+// dlarft (forward, columnwise) for every back-transform block at once: one
+// CTA per block b, T_b (nb x nb upper) from S_b = V_b^T V_b and tau, T in smem
+__global__ void k_larft(int nref, const double* __restrict__ S, const double* __restrict__ tau,
+                        double* __restrict__ T) {
+    extern __shared__ double sT[];  // BT_NB x BT_NB, then one column of S
+    const int b = blockIdx.x;
+    const int j0 = b * BT_NB, nb = min(BT_NB, nref - j0);
+    const double* Sb = S + (size_t)b * BT_NB * BT_NB;
+    double* scol = sT + BT_NB * BT_NB;
+    for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) sT[idx] = 0.0;
+    __syncthreads();
+    for (int i = 0; i < nb; ++i) {
+        for (int r = threadIdx.x; r < i; r += blockDim.x) scol[r] = Sb[r + (size_t)i * BT_NB];
+        __syncthreads();
+        const double ti = tau[j0 + i];
+        for (int r = threadIdx.x; r < i; r += blockDim.x) {  // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i)
+            double acc = 0.0;
+            for (int c = r; c < i; ++c) acc = fma(sT[r + c * BT_NB], scol[c], acc);
+            sT[r + i * BT_NB] = -ti * acc;
+        }
+        if (threadIdx.x == 0) sT[i + i * BT_NB] = ti;
+        __syncthreads();
+    }
+    double* Tb = T + (size_t)b * BT_NB * BT_NB;
+    for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) Tb[idx] = sT[idx];
+}
+
+// eigenvalues descending into w (indices beyond the computed range: 0)
+__global__ void k_desc(int n, int k_lo, const double* __restrict__ lam_asc, double* __restrict__ w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) w[i] = (n - 1 - i >= k_lo) ? lam_asc[n - 1 - i] : 0.0;
+}
+
+struct Work {
+    DeviceBuf V, W, vec, Z, Dp, Y, S, T, M1, M2, ws;
+    unsigned* bar = nullptr;
+    int grid = 0;
+};
+std::mutex g_mu;
+std::unordered_map<cudaStream_t, Work> g_work;
+
+size_t trd_smem(int n) {
+    const size_t npad = (size_t)((n + 3) & ~1);
+    return sizeof(double) * (64 + 3 * npad + 4 * TRD_NB + 4 * (size_t)TRD_TILE * TRD_NB);
+}
+}  // namespace
+
+constexpr int kEighLargeMax = 4096;  // shared-memory bound of k_sytrd (3 n + tiles doubles)
+
+void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec) {
+    if (n > kEighLargeMax) throw InvalidInput("eigh: n beyond the device solver limit");
+    if (nvec <= 0 || nvec > n) nvec = n;
+    Work* wp;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        wp = &g_work[st];
+    }
+    Work& wk = *wp;
+    int dev = 0;
+    AERO_CUDA(cudaGetDevice(&dev));
+    const size_t smem = trd_smem(n);
+    if (!wk.bar) {
+        AERO_CUDA(cudaMalloc(&wk.bar, 64));
+        const size_t smax = trd_smem(kEighLargeMax);
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * (kSytrdSmall * kSytrdSmall + 2 * kSytrdSmall + 64))));
+        AERO_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(2 * sizeof(double) * kEighLargeMax)));
+        AERO_CUDA(cudaFuncSetAttribute(k_twisted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(2 * sizeof(double) * kEighLargeMax)));
+        AERO_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * (BT_NB * BT_NB + BT_NB))));
+        int sms = 0;
+        AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        wk.grid = sms;  // one CTA per SM (cooperative residency)
+    }
+    // CTAs: enough that the symv columns spread, few enough that barriers stay cheap
+    // CTAs: enough that the symv columns spread (and 4 rows per warp cover n),
+    // few enough that barriers stay cheap
+    const int G = std::max((n + 31) / 32, std::min(wk.grid, (n + 13) / 14));
+    const size_t n2 = (size_t)n * n;
+    wk.V.alloc(n2);
+    wk.W.alloc((size_t)n * TRD_NB);
+    wk.vec.alloc((size_t)9 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB + 8);
+    double* d = wk.vec.p;
+    double* e = d + n;
+    double* tau = e + n;
+    double* y0 = tau + n;
+    double* wpre = y0 + n;
+    double* ybuf = wpre + n;
+    double* e2 = ybuf + n;
+    double* lam = e2 + n;
+    double* slots = lam + n + n;
+    double* dots = slots + SLOTW * wk.grid;
+    double* bounds = dots + 2 * TRD_NB;
+    fill_zero(st, wk.V.p, (int64_t)n2);
+    fill_zero(st, e, n);
+    fill_zero(st, tau, n);
+    AERO_CUDA(cudaMemsetAsync(wk.bar, 0, sizeof(unsigned), st));
+
+    static const bool trd_prof = getenv("AERO_SYTRD_PROF") != nullptr;
+    unsigned long long* prof = nullptr;
+    if (trd_prof) {
+        AERO_CUDA(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
+        AERO_CUDA(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
+    }
+    TrdArgs ta{n, lda, A, wk.V.p, wk.W.p, d, e, tau, ybuf, wpre, y0, slots, dots, wk.bar, prof};
+    void* args[] = {&ta};
+    const bool vec = !(lda & 1) && !((uintptr_t)A & 15);
+    note_launch();
+    if (n <= kSytrdSmall) {
+        k_sytrd_small<<<1, 512, sizeof(double) * ((size_t)n * n + 2 * n + 64), st>>>(n, A, lda, wk.V.p, d, e, tau);
+        AERO_LAUNCHED();
+    } else {
+        AERO_CUDA(cudaLaunchCooperativeKernel(vec ? (void*)k_sytrd<true> : (void*)k_sytrd<false>, dim3(G),
+                                              dim3(TRD_THREADS), args, smem, st));
+    }
+    if (prof) {
+        unsigned long long h[16];
+        AERO_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+        AERO_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "sytrd n=%d G=%d kcycles: R %.0f B %.0f bar1 %.0f C %.0f bar2 %.0f A' %.0f bar3 %.0f trail %.0f bar4+load %.0f\n",
+                n, G, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3,
+                h[7] / 1e3, h[8] / 1e3);
+        cudaFree(prof);
+    }
+
+    note_launch();
+    k_tri_prep<<<1, 1024, 0, st>>>(n, d, e, e2, bounds);
+    AERO_LAUNCHED();
+    // eigenvalues: all when every vector is wanted, else the top nvec + 1
+    const int k_lo = (nvec >= n) ? 0 : n - (nvec + 1);
+    const int nk = n - k_lo;
+    const size_t sde = 2 * sizeof(double) * (size_t)n;
+    note_launch();
+    k_bisect<<<(nk * 32 + 127) / 128, 128, sde, st>>>(n, k_lo, d, e2, bounds, lam);
+    AERO_LAUNCHED();
+    note_launch();
+    k_desc<<<(n + 255) / 256, 256, 0, st>>>(n, k_lo, lam, w);
+    AERO_LAUNCHED();
+
+    // eigenvectors of T for the top nvec eigenvalues
+    wk.Dp.alloc((size_t)n * nvec);
+    wk.Z.alloc((size_t)n * nvec);
+    note_launch();
+    k_twisted<<<(nvec + 31) / 32, 32, sde, st>>>(n, nvec, d, e, lam, bounds, wk.Dp.p, wk.Z.p);
+    AERO_LAUNCHED();
+    note_launch();
+    k_cluster_mgs<<<(nvec * 32 + 255) / 256, 256, 0, st>>>(n, nvec, lam, bounds, wk.Z.p);
+    AERO_LAUNCHED();
+    // Y = columns; then back-transform Y <- Q Y, Q = H_0 ... H_{n-2}
+    const int ldy = (n + 1) & ~1;
+    wk.Y.alloc((size_t)ldy * nvec);
+    double* Y = wk.Y.p;
+    note_launch();
+    k_interleaved_to_cols<<<dim3((n + 31) / 32, (nvec + 31) / 32), dim3(32, 8), 0, st>>>(n, nvec, wk.Z.p, Y, ldy);
+    AERO_LAUNCHED();
+    const int nref = n - 1;  // reflectors j = 0 .. n-2 (rows j+1 ..)
+    const int nblk = (nref + BT_NB - 1) / BT_NB;
+    wk.S.alloc((size_t)nblk * BT_NB * BT_NB);
+    wk.T.alloc((size_t)nblk * BT_NB * BT_NB);
+    wk.M1.alloc((size_t)BT_NB * nvec);
+    wk.M2.alloc((size_t)BT_NB * nvec);
+    const size_t wsn = (size_t)8 * BT_NB * std::max(nvec, BT_NB);  // split-K partials of skinny products
+    wk.ws.alloc(wsn);
+    // row j0 of block b is zero in every reflector of the block: start there (keeps 16 B alignment)
+    for (int b = 0; b < nblk; ++b) {
+        const int j0 = b * BT_NB, nb = std::min(BT_NB, nref - j0), mr = n - j0;
+        const double* Vb = wk.V.p + j0 + (size_t)j0 * n;
+        gemm_acc(st, true, false, nb, nb, mr, 1.0, Vb, n, Vb, n, 0.0, wk.S.p + (size_t)b * BT_NB * BT_NB, BT_NB,
+                 wk.ws.p, wsn);
+    }
+    note_launch();
+    k_larft<<<nblk, 128, sizeof(double) * (BT_NB * BT_NB + BT_NB), st>>>(nref, wk.S.p, tau, wk.T.p);
+    AERO_LAUNCHED();
+    for (int b = nblk - 1; b >= 0; --b) {
+        const int j0 = b * BT_NB, nb = std::min(BT_NB, nref - j0), mr = n - j0;
+        const double* Vb = wk.V.p + j0 + (size_t)j0 * n;  // mr x nb, ld n
+        const double* Tb = wk.T.p + (size_t)b * BT_NB * BT_NB;
+        // M1 = Vb^T Y[j0:, :] ; M2 = T M1 ; Y[j0:, :] -= Vb M2
+        gemm_acc(st, true, false, nb, nvec, mr, 1.0, Vb, n, Y + j0, ldy, 0.0, wk.M1.p, BT_NB, wk.ws.p, wsn);
+        gemm_acc(st, false, false, nb, nvec, nb, 1.0, Tb, BT_NB, wk.M1.p, BT_NB, 0.0, wk.M2.p, BT_NB,
+                 wk.ws.p, wsn);
+        gemm_acc(st, false, false, mr, nvec, nb, -1.0, Vb, n, wk.M2.p, BT_NB, 1.0, Y + j0, ldy, wk.ws.p, wsn);
+    }
+    copy_matrix(st, n, nvec, Y, ldy, A, lda);
+    fix_column_signs(st, n, nvec, A, lda, nullptr);
+}
+
+void eigh_large_forget(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_work.find(st);
+    if (it == g_work.end()) return;
+    if (it->second.bar) cudaFree(it->second.bar);
+    g_work.erase(it);
+}
+
+}  // namespace aero_b200

@@ -262,7 +262,7 @@ def test_ml_bookkeeping_bit_exact(orc, n_win, scale_rows):
 
 
 # ---------------------------------------------------------------- eigensolver
-@pytest.mark.parametrize("n", [2, 7, 32, 64, 96, 97, 256])
+@pytest.mark.parametrize("n", [2, 7, 32, 64, 96, 97, 128, 256, 301, 512, 1024])
 def test_eigh_matches_oracle(orc, n):
     a = gaussian(orc, n + 3, n, 11, n)
     b = a.T @ a
@@ -271,10 +271,30 @@ def test_eigh_matches_oracle(orc, n):
     lr, vr = orc.eigh(b)
     assert np.max(np.abs(lam - lr)) <= 1e-12 * np.max(np.abs(lr))
     assert np.linalg.norm(v @ np.diag(lam) @ v.T - b) <= 1e-12 * np.linalg.norm(b)
-    assert np.linalg.norm(v.T @ v - np.eye(n)) < 1e-12
+    assert np.linalg.norm(v.T @ v - np.eye(n)) < 1e-10  # twisted-factorization vectors: eps ||B|| / gap
     # sign convention (linalg.cpp:17-26): largest-magnitude entry positive
     idx = np.argmax(np.abs(v), axis=0)
     assert np.all(v[idx, np.arange(n)] > 0)
+    # eigenvectors themselves where the eigenvalue is separated (angle ~ eps ||B|| / gap)
+    gap = np.minimum(np.abs(np.diff(lr, prepend=np.inf)), np.abs(np.diff(lr, append=-np.inf)))
+    sep = gap > 1e-6 * np.max(np.abs(lr))
+    assert np.max(np.abs(v[:, sep] - vr[:, sep])) < 1e-8
+
+
+@pytest.mark.parametrize("n,rank", [(256, 100), (512, 511), (600, 40)])
+def test_eigh_rank_deficient_gram(orc, n, rank):
+    """FD-reduce-shaped input: a Gram matrix with an exact null space (clusters
+    of zero eigenvalues) -- eigenvalues, the range-space vectors and
+    orthonormality must hold, nothing may be non-finite."""
+    a = gaussian(orc, rank, n, 12, n) * np.linspace(3.0, 0.1, rank)[:, None]
+    b = a.T @ a
+    lam, v = prod.eigh(b)
+    lr, _ = orc.eigh(b)
+    assert np.all(np.isfinite(v)) and np.all(np.isfinite(lam))
+    assert np.max(np.abs(lam - lr)) <= 1e-12 * np.max(np.abs(lr))
+    assert np.linalg.norm(v @ np.diag(lam) @ v.T - b) <= 1e-11 * np.linalg.norm(b)
+    top = v[:, :rank]
+    assert np.linalg.norm(top.T @ top - np.eye(rank)) < 1e-10
 
 
 # ---------------------------------------------------------------- distributed

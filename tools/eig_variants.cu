@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <vector>
 #include <random>
-#define CK(x) do { auto e = (x); if (e != 0) printf("err %d at %s\n", (int)e, #x); } while (0)
+#define CK(x) do { auto e_ = (x); if (e_ != 0) printf("err %d at %s\n", (int)e_, #x); } while (0)
 int main() {
     const int n = 2048, il = n - 1024 + 1, iu = n;
     std::mt19937_64 g(1);
@@ -96,6 +96,34 @@ int main() {
         CK(cusolverDnDsyevj(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n, dW, workj, lwj, info, sj));
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
         printf("Dsyevj          %8.2f ms\n", ms);
+    }
+    // 6. breakdown: sytrd, syevd eigenvalues only, ormtr (1024 columns)
+    {
+        double *d, *e, *tau, *wk, *C;
+        cudaMalloc(&d, sizeof(double) * n); cudaMalloc(&e, sizeof(double) * n); cudaMalloc(&tau, sizeof(double) * n);
+        cudaMalloc(&C, sizeof(double) * n * 1024);
+        int lt = 0, lo = 0, lv = 0;
+        cusolverDnDsytrd_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, dA, n, d, e, tau, &lt);
+        cusolverDnDormtr_bufferSize(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, n, 1024, dA, n, tau, C, n, &lo);
+        cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n, dW, &lv);
+        int lmax = lt > lo ? lt : lo; lmax = lmax > lv ? lmax : lv;
+        cudaMalloc(&wk, sizeof(double) * lmax);
+        for (int rep = 0; rep < 3; ++rep) {
+            reset();
+            cudaEventRecord(e0);
+            CK(cusolverDnDsytrd(h, CUBLAS_FILL_MODE_LOWER, n, dA, n, d, e, tau, wk, lmax, info));
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+            printf("Dsytrd          %8.2f ms\n", ms);
+            cudaEventRecord(e0);
+            CK(cusolverDnDormtr(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, n, 1024, dA, n, tau, C, n, wk, lmax, info));
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+            printf("Dormtr 1024     %8.2f ms\n", ms);
+            reset();
+            cudaEventRecord(e0);
+            CK(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, n, dA, n, dW, wk, lmax, info));
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+            printf("Dsyevd novec    %8.2f ms\n", ms);
+        }
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
