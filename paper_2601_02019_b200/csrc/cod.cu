@@ -295,7 +295,16 @@ __device__ void cta_eig_small(double* W, double* V, int k, double* cs) {
     __syncthreads();
 }
 
+// G[c0 + j, i] = G[i, c0 + j] for i < c0 (mirror the appended columns into rows)
+__global__ void k_cod_mirror(int c0, int nb, double* G, int ld) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)c0 * nb) return;
+    const int i = (int)(e % c0), j = (int)(e / c0);
+    G[(c0 + j) + (int64_t)i * ld] = G[i + (int64_t)(c0 + j) * ld];
+}
 }  // namespace
+
+constexpr int COD_MAX_BATCH = 128;  // speculative gate jobs per launch
 
 struct CodSnap {
     int xi;
@@ -310,7 +319,9 @@ struct CodEngine::Impl {
     uint64_t seed, stream, forks = 0;
     int c = 0;
     cudaStream_t st = nullptr;
-    DeviceBuf A, B, GA, GB, A2, B2, sig, hv, work, ws, q1, q2, q3, pib;
+    DeviceBuf A, B, GA, GB, A2, B2, sig, hv, work, ws, q1, q2, q3, pib, xs_d, ys_d, gws;
+    int batch = 32;         // adaptive speculative batch (rows)
+    double fire_ema = 0.0;  // moving average of gate fires (batch pattern prediction)
     CodJob* jobs_d = nullptr;
     int* status_d = nullptr;
     std::deque<CodSnap> snaps;
@@ -319,12 +330,30 @@ struct CodEngine::Impl {
     uint64_t fork_state(uint64_t f) const { return rng_state0(seed, fork_stream(stream, f)); }
 
     void regram() {  // GA = A^T A, GB = B^T B
-        dgemm(st, true, false, c, c, dx, 1.0, A.p, dx, A.p, dx, 0.0, GA.p, cap);
-        dgemm(st, true, false, c, c, dy, 1.0, B.p, dy, B.p, dy, 0.0, GB.p, cap);
+        gemm_acc(st, true, false, c, c, dx, 1.0, A.p, dx, A.p, dx, 0.0, GA.p, cap, gws.p, gws.n);
+        gemm_acc(st, true, false, c, c, dy, 1.0, B.p, dy, B.p, dy, 0.0, GB.p, cap, gws.p, gws.n);
+    }
+    // append nb columns (device, contiguous) at c and extend the Grams by the
+    // new column block (GA[0:c+nb, c:c+nb] = A^T x_new) and its mirror
+    void append(const double* xd, const double* yd, int nb) {
+        AERO_CUDA(cudaMemcpyAsync(A.p + (size_t)c * dx, xd, sizeof(double) * dx * nb, cudaMemcpyDeviceToDevice, st));
+        AERO_CUDA(cudaMemcpyAsync(B.p + (size_t)c * dy, yd, sizeof(double) * dy * nb, cudaMemcpyDeviceToDevice, st));
+        gemm_acc(st, true, false, c + nb, nb, dx, 1.0, A.p, dx, A.p + (size_t)c * dx, dx, 0.0, GA.p + (size_t)c * cap,
+                 cap, gws.p, gws.n);
+        gemm_acc(st, true, false, c + nb, nb, dy, 1.0, B.p, dy, B.p + (size_t)c * dy, dy, 0.0, GB.p + (size_t)c * cap,
+                 cap, gws.p, gws.n);
+        if (c > 0) {
+            const int64_t tot = (int64_t)c * nb;
+            k_cod_mirror<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c, nb, GA.p, cap);
+            AERO_LAUNCHED();
+            k_cod_mirror<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c, nb, GB.p, cap);
+            AERO_LAUNCHED();
+        }
+        c += nb;
     }
 
     // run jobs (<= 3) -> sig (host), status (host)
-    void run(CodJob* hj, int nj, double* sig_h, int* status_h) {
+    void run(const CodJob* hj, int nj, double* sig_h, int* status_h) {
         AERO_CUDA(cudaMemcpyAsync(jobs_d, hj, sizeof(CodJob) * nj, cudaMemcpyHostToDevice, st));
         const size_t smem = sizeof(double) * (32 + 2 * (size_t)c * COD_KMAX + 3 * COD_KMAX * COD_KMAX +
                                               COD_KMAX + 64) + 16;
@@ -335,7 +364,7 @@ struct CodEngine::Impl {
             attr = true;
         }
         const int64_t pis = (int64_t)std::max(dx, dy) * COD_KMAX;
-        pib.alloc((size_t)3 * pis);
+        pib.alloc((size_t)std::max(nj, 3) * pis);
         k_cod_job<<<nj, 256, smem, st>>>(jobs_d, A.p, dx, B.p, dy, GA.p, GB.p, cap, sig.p, hv.p,
                                          status_d, pib.p, pis);
         AERO_LAUNCHED();
@@ -486,10 +515,11 @@ CodEngine::CodEngine(int dx, int dy, double eps, double theta, int64_t n, uint64
     s.B2.alloc((size_t)dy * s.cap);
     s.GA.alloc((size_t)s.cap * s.cap);
     s.GB.alloc((size_t)s.cap * s.cap);
-    s.sig.alloc(3 * COD_KMAX);
-    s.hv.alloc((size_t)3 * s.cap * COD_KMAX);
-    AERO_CUDA(cudaMalloc(&s.jobs_d, sizeof(CodJob) * 3));
-    AERO_CUDA(cudaMalloc(&s.status_d, sizeof(int) * 3));
+    s.sig.alloc((size_t)COD_MAX_BATCH * COD_KMAX);
+    s.hv.alloc((size_t)COD_MAX_BATCH * s.cap * COD_KMAX);
+    s.gws.alloc((size_t)8 * s.cap * COD_MAX_BATCH);
+    AERO_CUDA(cudaMalloc(&s.jobs_d, sizeof(CodJob) * COD_MAX_BATCH));
+    AERO_CUDA(cudaMalloc(&s.status_d, sizeof(int) * COD_MAX_BATCH));
 }
 
 CodEngine::~CodEngine() {
@@ -511,25 +541,41 @@ CodEngine::~CodEngine() {
     delete im_;
 }
 
-// amm.cpp:42-103, one (x, y) pair at a time
+// amm.cpp:42-103. Rows are applied in speculative batches: the columns of a
+// batch are appended at once (Gram column block by one GEMM), the gates of all
+// its rows run as one launch (row j's gate sees the buffer prefix c0 + j + 1
+// and fork F + j + 1, exactly what it would see one row at a time if no
+// earlier row of the batch fired). The first row whose gate fires is finished
+// exactly (paired simul_iter, doubling, dump) and ends the batch; the row that
+// fills the buffer (reduce before its gate) always runs alone.
 void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, const int64_t* t,
                              aero_event* log) {
     Impl& s = *im_;
     AERO_CUDA(cudaSetDevice(s.dev));
-    for (int64_t q = 0; q < nrows; ++q) {
-        const double* x = xs + q * s.dx;
-        const double* y = ys + q * s.dy;
-        for (int j = 0; j < s.dx; ++j)
-            if (!std::isfinite(x[j])) throw InvalidInput("CodState: non-finite input");
-        for (int j = 0; j < s.dy; ++j)
-            if (!std::isfinite(y[j])) throw InvalidInput("CodState: non-finite input");
-        const int64_t i = t[q];
-        if (i <= s.clock) throw InvalidInput("CodState: timestamp regression");
-        aero_event ev{};
-        ev.t = i;
-        ev.theta = s.theta;
-        ev.forks_before = (int64_t)s.forks;
-        // expire (amm.cpp:48)
+    if (nrows <= 0) return;
+    int64_t good = nrows;
+    std::string err;
+    int64_t prev = s.clock;
+    for (int64_t q = 0; q < nrows && err.empty(); ++q) {
+        for (int j = 0; j < s.dx && err.empty(); ++j)
+            if (!std::isfinite(xs[q * s.dx + j])) err = "CodState: non-finite input";
+        for (int j = 0; j < s.dy && err.empty(); ++j)
+            if (!std::isfinite(ys[q * s.dy + j])) err = "CodState: non-finite input";
+        if (err.empty() && t[q] <= prev) err = "CodState: timestamp regression";
+        if (!err.empty()) good = q;
+        prev = t[q];
+    }
+    if (good > 0) {
+        s.xs_d.alloc((size_t)good * s.dx);
+        s.ys_d.alloc((size_t)good * s.dy);
+        AERO_CUDA(cudaMemcpyAsync(s.xs_d.p, xs, sizeof(double) * good * s.dx, cudaMemcpyHostToDevice, s.st));
+        AERO_CUDA(cudaMemcpyAsync(s.ys_d.p, ys, sizeof(double) * good * s.dy, cudaMemcpyHostToDevice, s.st));
+    }
+    std::vector<double> sig_h((size_t)COD_MAX_BATCH * COD_KMAX);
+    std::vector<int> status_h(COD_MAX_BATCH);
+    std::vector<CodJob> jobs(COD_MAX_BATCH);
+
+    auto expire = [&](int64_t i) {  // amm.cpp:48
         while (!s.snaps.empty() && s.snaps.front().t + s.n <= i) {
             AERO_CUDA(cudaStreamSynchronize(s.st));
             auto& f = s.snaps.front();
@@ -539,99 +585,206 @@ void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, 
             cudaFree(f.mh);
             s.snaps.pop_front();
         }
-        // append the column pair (amm.cpp:51-54) and the new Gram row/column
-        AERO_CUDA(cudaMemcpyAsync(s.A.p + (size_t)s.c * s.dx, x, sizeof(double) * s.dx, cudaMemcpyHostToDevice, s.st));
-        AERO_CUDA(cudaMemcpyAsync(s.B.p + (size_t)s.c * s.dy, y, sizeof(double) * s.dy, cudaMemcpyHostToDevice, s.st));
-        s.c += 1;
-        s.regram();
-        if (s.c == s.cap) {  // amm.cpp:56-62
-            s.cod_reduce();
-            ev.reduced = 1;
-        }
-        // gate (amm.cpp:65-71): sigma1 = sqrt(power_iteration(p, kp).first)
+    };
+    // the gate fired (amm.cpp:72-101): paired simul_iter with doubling, dump
+    // pre: results of the first (k = min(2, kmax)) simul pair when the batch
+    // already ran it (z sigma_hat, z status, z / h c-space bases), else null
+    auto fired = [&](int64_t i, aero_event& ev, const double* pre_sz, int pre_stz, const double* pre_hvz,
+                     const double* pre_hvh) {
         double sig[3 * COD_KMAX];
         int status[3];
-        CodJob gj{0, s.c, 1, s.kp, s.fork_state(++s.forks)};
-        s.run(&gj, 1, sig, status);
-        const double s1sq = (status[0] == JOB_ACTIVE) ? sig[0] : 0.0;
-        const double sigma1 = std::sqrt(s1sq);
-        ev.sigma1_sq = s1sq;
-        if (!(sigma1 < 0.5 * s.theta)) {
-            ev.gate_fired = 1;
-            const int kmax = std::min({s.ell, s.dx, s.dy, s.c});
-            int k = std::min(2, kmax);
-            while (true) {
-                ev.doubling_steps++;
-                ev.simul_calls += 2;
-                if (k > COD_KMAX) throw InvalidInput("CodState: rank beyond the in-kernel limit");
+        ev.gate_fired = 1;
+        const int kmax = std::min({s.ell, s.dx, s.dy, s.c});
+        int k = std::min(2, kmax);
+        bool have = pre_sz != nullptr;
+        while (true) {
+            ev.doubling_steps++;
+            ev.simul_calls += 2;
+            if (k > COD_KMAX) throw InvalidInput("CodState: rank beyond the in-kernel limit");
+            const double* sz;  // z side sigma_hat
+            const double* hvz;
+            const double* hvh;
+            int stz;
+            if (have) {
+                sz = pre_sz;
+                stz = pre_stz;
+                hvz = pre_hvz;
+                hvh = pre_hvh;
+                have = false;
+            } else {
                 CodJob jz{1, s.c, k, s.qz, s.fork_state(++s.forks)};
                 CodJob jh{2, s.c, k, s.qh, s.fork_state(++s.forks)};
                 CodJob js[2] = {jz, jh};
                 s.run(js, 2, sig, status);
-                const double* sz = sig;  // z side sigma_hat
-                ev.k_last = k;
-                ev.tail_sq = sz[k - 1];
-                if (sz[k - 1] < s.theta || k == kmax) {
-                    int xi = 0;
-                    for (int j = 0; j < k; ++j) {
-                        if (sz[j] >= s.theta) xi = j + 1;
-                        else break;
-                    }
-                    ev.xi = xi;
-                    if (xi >= 1) {
-                        CodSnap sn{};
-                        sn.xi = xi;
-                        AERO_CUDA(cudaMalloc(&sn.z, sizeof(double) * s.dx * xi));
-                        AERO_CUDA(cudaMalloc(&sn.h, sizeof(double) * s.dy * xi));
-                        AERO_CUDA(cudaMalloc(&sn.zm_t, sizeof(double) * s.dy * xi));
-                        AERO_CUDA(cudaMalloc(&sn.mh, sizeof(double) * s.dx * xi));
-                        const double* hvz = s.hv.p;
-                        const double* hvh = s.hv.p + (size_t)s.cap * COD_KMAX;
-                        if (status[0] == JOB_ZERO) {
-                            std::vector<double> I((size_t)s.dx * xi, 0.0), J((size_t)s.dy * xi, 0.0);
-                            for (int j = 0; j < xi; ++j) {
-                                if (j < s.dx) I[j + (size_t)j * s.dx] = 1.0;
-                                if (j < s.dy) J[j + (size_t)j * s.dy] = 1.0;
-                            }
-                            AERO_CUDA(cudaMemcpyAsync(sn.z, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, s.st));
-                            AERO_CUDA(cudaMemcpyAsync(sn.h, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, s.st));
-                        } else {
-                            dgemm(s.st, false, false, s.dx, xi, s.c, 1.0, s.A.p, s.dx, hvz, s.cap, 0.0, sn.z, s.dx);
-                            dgemm(s.st, false, false, s.dy, xi, s.c, 1.0, s.B.p, s.dy, hvh, s.cap, 0.0, sn.h, s.dy);
-                            fix_column_signs(s.st, s.dx, xi, sn.z, s.dx, nullptr);
-                            fix_column_signs(s.st, s.dy, xi, sn.h, s.dy, nullptr);
-                        }
-                        // zm = z^T p = (z^T A) B^T ; mh = p h = A (B^T h)   (amm.cpp:87-88)
-                        s.work.alloc((size_t)2 * s.cap * xi + 64);
-                        double* zA = s.work.p;                 // xi x c (ld xi)
-                        double* Bh = zA + (size_t)s.cap * xi;  // c x xi (ld cap)
-                        dgemm(s.st, true, false, xi, s.c, s.dx, 1.0, sn.z, s.dx, s.A.p, s.dx, 0.0, zA, xi);
-                        dgemm(s.st, true, false, s.c, xi, s.dy, 1.0, s.B.p, s.dy, sn.h, s.dy, 0.0, Bh, s.cap);
-                        dgemm(s.st, false, true, s.dy, xi, s.c, 1.0, s.B.p, s.dy, zA, xi, 0.0, sn.zm_t, s.dy);
-                        dgemm(s.st, false, false, s.dx, xi, s.c, 1.0, s.A.p, s.dx, Bh, s.cap, 0.0, sn.mh, s.dx);
-                        // A -= z (z^T A), B -= h (h^T B)   (amm.cpp:92-93)
-                        dgemm(s.st, false, false, s.dx, s.c, xi, -1.0, sn.z, s.dx, zA, xi, 1.0, s.A.p, s.dx);
-                        dgemm(s.st, true, false, xi, s.c, s.dy, 1.0, sn.h, s.dy, s.B.p, s.dy, 0.0, zA, xi);
-                        dgemm(s.st, false, false, s.dy, s.c, xi, -1.0, sn.h, s.dy, zA, xi, 1.0, s.B.p, s.dy);
-                        s.regram();
-                        sn.s = s.last_dump + 1;
-                        sn.t = i;
-                        s.last_dump = i;
-                        s.snaps.push_back(sn);
-                        ev.dumped = 1;
-                    }
-                    break;
-                }
-                k = std::min(2 * k, kmax);
+                sz = sig;
+                stz = status[0];
+                hvz = s.hv.p;
+                hvh = s.hv.p + (size_t)s.cap * COD_KMAX;
             }
+            ev.k_last = k;
+            ev.tail_sq = sz[k - 1];
+            if (sz[k - 1] < s.theta || k == kmax) {
+                int xi = 0;
+                for (int j = 0; j < k; ++j) {
+                    if (sz[j] >= s.theta) xi = j + 1;
+                    else break;
+                }
+                ev.xi = xi;
+                if (xi >= 1) {
+                    CodSnap sn{};
+                    sn.xi = xi;
+                    AERO_CUDA(cudaMalloc(&sn.z, sizeof(double) * s.dx * xi));
+                    AERO_CUDA(cudaMalloc(&sn.h, sizeof(double) * s.dy * xi));
+                    AERO_CUDA(cudaMalloc(&sn.zm_t, sizeof(double) * s.dy * xi));
+                    AERO_CUDA(cudaMalloc(&sn.mh, sizeof(double) * s.dx * xi));
+                    if (stz == JOB_ZERO) {
+                        std::vector<double> I((size_t)s.dx * xi, 0.0), J((size_t)s.dy * xi, 0.0);
+                        for (int j = 0; j < xi; ++j) {
+                            if (j < s.dx) I[j + (size_t)j * s.dx] = 1.0;
+                            if (j < s.dy) J[j + (size_t)j * s.dy] = 1.0;
+                        }
+                        AERO_CUDA(cudaMemcpyAsync(sn.z, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, s.st));
+                        AERO_CUDA(cudaMemcpyAsync(sn.h, J.data(), sizeof(double) * J.size(), cudaMemcpyHostToDevice, s.st));
+                        AERO_CUDA(cudaStreamSynchronize(s.st));
+                    } else {
+                        dgemm(s.st, false, false, s.dx, xi, s.c, 1.0, s.A.p, s.dx, hvz, s.cap, 0.0, sn.z, s.dx);
+                        dgemm(s.st, false, false, s.dy, xi, s.c, 1.0, s.B.p, s.dy, hvh, s.cap, 0.0, sn.h, s.dy);
+                        fix_column_signs(s.st, s.dx, xi, sn.z, s.dx, nullptr);
+                        fix_column_signs(s.st, s.dy, xi, sn.h, s.dy, nullptr);
+                    }
+                    // zm = z^T p = (z^T A) B^T ; mh = p h = A (B^T h)   (amm.cpp:87-88)
+                    s.work.alloc((size_t)2 * s.cap * xi + 64);
+                    double* zA = s.work.p;                 // xi x c (ld xi)
+                    double* Bh = zA + (size_t)s.cap * xi;  // c x xi (ld cap)
+                    dgemm(s.st, true, false, xi, s.c, s.dx, 1.0, sn.z, s.dx, s.A.p, s.dx, 0.0, zA, xi);
+                    dgemm(s.st, true, false, s.c, xi, s.dy, 1.0, s.B.p, s.dy, sn.h, s.dy, 0.0, Bh, s.cap);
+                    dgemm(s.st, false, true, s.dy, xi, s.c, 1.0, s.B.p, s.dy, zA, xi, 0.0, sn.zm_t, s.dy);
+                    dgemm(s.st, false, false, s.dx, xi, s.c, 1.0, s.A.p, s.dx, Bh, s.cap, 0.0, sn.mh, s.dx);
+                    // A -= z (z^T A), B -= h (h^T B)   (amm.cpp:92-93)
+                    dgemm(s.st, false, false, s.dx, s.c, xi, -1.0, sn.z, s.dx, zA, xi, 1.0, s.A.p, s.dx);
+                    dgemm(s.st, true, false, xi, s.c, s.dy, 1.0, sn.h, s.dy, s.B.p, s.dy, 0.0, zA, xi);
+                    dgemm(s.st, false, false, s.dy, s.c, xi, -1.0, sn.h, s.dy, zA, xi, 1.0, s.B.p, s.dy);
+                    s.regram();
+                    sn.s = s.last_dump + 1;
+                    sn.t = i;
+                    s.last_dump = i;
+                    s.snaps.push_back(sn);
+                    ev.dumped = 1;
+                }
+                break;
+            }
+            k = std::min(2 * k, kmax);
         }
-        s.clock = i;
+    };
+    auto finish = [&](int64_t q, aero_event& ev) {
+        s.clock = t[q];
         ev.forks_after = (int64_t)s.forks;
         ev.rows_after = s.c;
         s.ev = ev;
         if (log) log[q] = ev;
+    };
+
+    int64_t q = 0;
+    while (q < good) {
+        const int room = s.cap - s.c;
+        const int nb = (int)std::min<int64_t>({(int64_t)s.batch, good - q, (int64_t)room - 1});
+        if (nb <= 0) {  // this row fills the buffer: append, reduce, then its gate
+            const int64_t i = t[q];
+            aero_event ev{};
+            ev.t = i;
+            ev.theta = s.theta;
+            ev.forks_before = (int64_t)s.forks;
+            expire(i);
+            s.append(s.xs_d.p + (size_t)q * s.dx, s.ys_d.p + (size_t)q * s.dy, 1);
+            if (s.c == s.cap) {  // amm.cpp:56-62
+                s.cod_reduce();
+                ev.reduced = 1;
+            }
+            CodJob gj{0, s.c, 1, s.kp, s.fork_state(++s.forks)};
+            s.run(&gj, 1, sig_h.data(), status_h.data());
+            const double s1sq = (status_h[0] == JOB_ACTIVE) ? sig_h[0] : 0.0;
+            ev.sigma1_sq = s1sq;
+            if (!(std::sqrt(s1sq) < 0.5 * s.theta)) fired(i, ev, nullptr, 0, nullptr, nullptr);
+            s.fire_ema = 0.9 * s.fire_ema + 0.1 * ev.gate_fired;
+            finish(q, ev);
+            ++q;
+            continue;
+        }
+        if (s.fire_ema > 0.5) {  // FIRE1 prediction: gate fires, one k = 2 pair, no dump
+            const int c0 = s.c;
+            const uint64_t F = s.forks;
+            const int nbf = std::min(nb, COD_MAX_BATCH / 3);
+            s.append(s.xs_d.p + (size_t)q * s.dx, s.ys_d.p + (size_t)q * s.dy, nbf);
+            for (int j = 0; j < nbf; ++j) {
+                const int cj = c0 + j + 1;
+                const int kj = std::min({2, s.ell, s.dx, s.dy, cj});
+                jobs[3 * j] = CodJob{0, cj, 1, s.kp, s.fork_state(F + 3 * j + 1)};
+                jobs[3 * j + 1] = CodJob{1, cj, kj, s.qz, s.fork_state(F + 3 * j + 2)};
+                jobs[3 * j + 2] = CodJob{2, cj, kj, s.qh, s.fork_state(F + 3 * j + 3)};
+            }
+            s.run(jobs.data(), 3 * nbf, sig_h.data(), status_h.data());
+            int j = 0;
+            bool deviated = false;
+            for (; j < nbf && !deviated; ++j) {
+                const int64_t i = t[q + j];
+                aero_event ev{};
+                ev.t = i;
+                ev.theta = s.theta;
+                ev.forks_before = (int64_t)(F + 3 * j);
+                expire(i);
+                s.c = c0 + j + 1;
+                s.forks = F + 3 * j + 1;
+                const double s1sq = (status_h[3 * j] == JOB_ACTIVE) ? sig_h[(size_t)3 * j * COD_KMAX] : 0.0;
+                ev.sigma1_sq = s1sq;
+                if (!(std::sqrt(s1sq) < 0.5 * s.theta)) {
+                    s.forks = F + 3 * j + 3;  // the pair of this row ran in the batch
+                    const double* sz = sig_h.data() + (size_t)(3 * j + 1) * COD_KMAX;
+                    const int kmax = std::min({s.ell, s.dx, s.dy, s.c});
+                    const int k = std::min(2, kmax);
+                    const bool settled = sz[k - 1] < s.theta || k == kmax;
+                    if (!settled || sz[0] >= s.theta) deviated = true;  // doubling or a dump ends the batch
+                    fired(i, ev, sz, status_h[3 * j + 1], s.hv.p + (size_t)(3 * j + 1) * s.cap * COD_KMAX,
+                          s.hv.p + (size_t)(3 * j + 2) * s.cap * COD_KMAX);
+                } else {
+                    deviated = true;  // predicted fire, gate stayed quiet: later forks shift
+                }
+                s.fire_ema = 0.9 * s.fire_ema + 0.1 * ev.gate_fired;
+                finish(q + j, ev);
+            }
+            q += j;
+            s.batch = deviated ? std::max(4, 2 * j) : std::min(COD_MAX_BATCH, 2 * s.batch);
+            continue;
+        }
+        const int c0 = s.c;
+        const uint64_t F = s.forks;
+        s.append(s.xs_d.p + (size_t)q * s.dx, s.ys_d.p + (size_t)q * s.dy, nb);
+        for (int j = 0; j < nb; ++j) jobs[j] = CodJob{0, c0 + j + 1, 1, s.kp, s.fork_state(F + j + 1)};
+        s.run(jobs.data(), nb, sig_h.data(), status_h.data());
+        int fire = -1;
+        for (int j = 0; j < nb && fire < 0; ++j) {
+            const double s1sq = (status_h[j] == JOB_ACTIVE) ? sig_h[(size_t)j * COD_KMAX] : 0.0;
+            if (!(std::sqrt(s1sq) < 0.5 * s.theta)) fire = j;
+        }
+        const int ncommit = (fire < 0) ? nb : fire + 1;
+        for (int j = 0; j < ncommit; ++j) {
+            const int64_t i = t[q + j];
+            aero_event ev{};
+            ev.t = i;
+            ev.theta = s.theta;
+            ev.forks_before = (int64_t)(F + j);
+            expire(i);
+            s.c = c0 + j + 1;
+            s.forks = F + j + 1;
+            ev.sigma1_sq = (status_h[j] == JOB_ACTIVE) ? sig_h[(size_t)j * COD_KMAX] : 0.0;
+            if (j == fire) fired(i, ev, nullptr, 0, nullptr, nullptr);
+            s.fire_ema = 0.9 * s.fire_ema + 0.1 * ev.gate_fired;
+            finish(q + j, ev);
+        }
+        q += ncommit;
+        s.batch = (fire < 0) ? std::min(COD_MAX_BATCH, 2 * s.batch) : std::max(4, 2 * (fire + 1));
     }
     AERO_CUDA(cudaStreamSynchronize(s.st));
+    if (good < nrows) throw InvalidInput(err);
 }
 
 // amm.cpp:105-114: p = A B^T + sum of cod_restore_contribution (amm.cpp:22-25)

@@ -14,7 +14,7 @@
 //  3. k_twisted -- eigenvectors of T for the top `nvec` eigenvalues from a
 //                  twisted LDL^T/UDU^T factorization (one thread per vector,
 //                  row-interleaved scratch so the qd sweeps coalesce), then
-//                  modified Gram-Schmidt inside tight clusters.
+//                  Gram-Schmidt (twice) inside tight clusters.
 //  4. back-transform Z = Q Y with compact-WY blocks of 128 reflectors
 //                  (T factor per block, three fp64 GEMMs on the product engine).
 // Output convention of eigh(): eigenvalues descending, eigenvector columns
@@ -649,32 +649,50 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     for (int i = 0; i < n; ++i) Z[(int64_t)i * nvec + q] *= s;
 }
 
-// modified Gram-Schmidt inside clusters of close eigenvalues (one warp per
-// cluster leader; clusters longer than kMaxCluster are left as computed)
+// re-orthonormalize the vectors of each cluster of close eigenvalues
+// (classical Gram-Schmidt applied twice, one CTA per cluster leader; clusters
+// longer than kMaxCluster are cut into consecutive groups of that length)
 constexpr int kMaxCluster = 128;
-__global__ void k_cluster_mgs(int n, int nvec, const double* __restrict__ lam_asc,
-                              const double* __restrict__ bounds, double* __restrict__ Z) {
-    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= nvec) return;
+__global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const double* __restrict__ lam_asc,
+                                                      const double* __restrict__ bounds, double* __restrict__ Z) {
+    __shared__ double dots[kMaxCluster];
+    __shared__ double red[64];
+    const int q = blockIdx.x;
     const double thr = 1e-7 * bounds[3] + bounds[2];
     auto lam = [&](int i) { return lam_asc[n - 1 - i]; };  // descending
-    if (q > 0 && lam(q - 1) - lam(q) <= thr) return;        // not a leader
+    auto linked = [&](int i) { return i > 0 && lam(i - 1) - lam(i) <= thr; };
+    if (linked(q)) {  // leader of a later group of a long cluster?
+        int st = q;
+        while (st > 0 && linked(st)) --st;
+        if ((q - st) % kMaxCluster != 0) return;
+    }
     int end = q + 1;
-    while (end < nvec && lam(end - 1) - lam(end) <= thr && end - q < kMaxCluster) ++end;
+    while (end < nvec && linked(end) && end - q < kMaxCluster) ++end;
     if (end - q < 2) return;
-    for (int i = q; i < end; ++i) {
-        for (int p = q; p < i; ++p) {
-            double dot = 0.0;
-            for (int t = lane; t < n; t += 32) dot += Z[(int64_t)t * nvec + p] * Z[(int64_t)t * nvec + i];
-            dot = warp_sum_d(dot);
-            for (int t = lane; t < n; t += 32) Z[(int64_t)t * nvec + i] -= dot * Z[(int64_t)t * nvec + p];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = q + 1; i < end; ++i) {
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int p = q + warp; p < i; p += 8) {
+                double dot = 0.0;
+                for (int t = lane; t < n; t += 32) dot = fma(Z[(int64_t)t * nvec + p], Z[(int64_t)t * nvec + i], dot);
+                dot = warp_sum_d(dot);
+                if (lane == 0) dots[p - q] = dot;
+            }
+            __syncthreads();
+            for (int t = tid; t < n; t += blockDim.x) {
+                const double* zr = Z + (int64_t)t * nvec;
+                double acc = zr[i];
+                for (int p = q; p < i; ++p) acc = fma(-dots[p - q], zr[p], acc);
+                Z[(int64_t)t * nvec + i] = acc;
+            }
+            __syncthreads();
         }
         double nr = 0.0;
-        for (int t = lane; t < n; t += 32) nr += Z[(int64_t)t * nvec + i] * Z[(int64_t)t * nvec + i];
-        nr = warp_sum_d(nr);
-        const double s = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
-        for (int t = lane; t < n; t += 32) Z[(int64_t)t * nvec + i] *= s;
+        for (int t = tid; t < n; t += blockDim.x) nr += Z[(int64_t)t * nvec + i] * Z[(int64_t)t * nvec + i];
+        nr = block_sum_d(nr, red);
+        const double sc = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+        for (int t = tid; t < n; t += blockDim.x) Z[(int64_t)t * nvec + i] *= sc;
+        __syncthreads();
     }
 }
 
@@ -844,7 +862,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     k_twisted<<<(nvec + 31) / 32, 32, sde, st>>>(n, nvec, d, e, lam, bounds, wk.Dp.p, wk.Z.p);
     AERO_LAUNCHED();
     note_launch();
-    k_cluster_mgs<<<(nvec * 32 + 255) / 256, 256, 0, st>>>(n, nvec, lam, bounds, wk.Z.p);
+    k_cluster_orth<<<nvec, 256, 0, st>>>(n, nvec, lam, bounds, wk.Z.p);
     AERO_LAUNCHED();
     // Y = columns; then back-transform Y <- Q Y, Q = H_0 ... H_{n-2}
     const int ldy = (n + 1) & ~1;
