@@ -32,24 +32,56 @@ struct CodJob {
     uint64_t rng0;
 };
 
-// y[0:c, 0:k] = G[0:c, 0:c] x[0:c, 0:k] (G global column-major ld, x/y shared, ld c)
+constexpr int COD_THREADS = 512;
+constexpr int COD_MV_PARTS = 2;  // threads per output row in cta_matvec (split over l)
+
+// y[0:c, 0:k] = G[0:c, 0:c] x[0:c, 0:k] (G global column-major ld, x/y shared,
+// ld c). Each output row is shared by COD_MV_PARTS threads over l, 8 loads in
+// flight per thread; `part` holds (parts-1) * (blockDim/parts) * COD_KMAX doubles.
 __device__ void cta_matvec(const double* __restrict__ G, int ld, int c, int k, const double* x,
-                           double* y) {
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
+                           double* y, double* part) {
+    const int R = blockDim.x / COD_MV_PARTS;
+    const int ii = threadIdx.x % R, p = threadIdx.x / R;
+    const int l0 = (c * p) / COD_MV_PARTS, l1 = (c * (p + 1)) / COD_MV_PARTS;
+    for (int i0 = 0; i0 < c; i0 += R) {
+        const int i = i0 + ii;
         double acc[COD_KMAX];
 #pragma unroll
         for (int j = 0; j < COD_KMAX; ++j) acc[j] = 0.0;
-        for (int l = 0; l < c; ++l) {
-            const double g = G[i + (int64_t)l * ld];
+        if (i < c) {
+            int l = l0;
+            for (; l + 8 <= l1; l += 8) {
+                double g[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) g[u] = G[i + (int64_t)(l + u) * ld];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int j = 0; j < COD_KMAX; ++j)
+                        if (j < k) acc[j] = fma(g[u], x[l + u + j * c], acc[j]);
+            }
+            for (; l < l1; ++l) {
+                const double g = G[i + (int64_t)l * ld];
+#pragma unroll
+                for (int j = 0; j < COD_KMAX; ++j)
+                    if (j < k) acc[j] = fma(g, x[l + j * c], acc[j]);
+            }
+        }
+        if (p > 0 && i < c)
 #pragma unroll
             for (int j = 0; j < COD_KMAX; ++j)
-                if (j < k) acc[j] = fma(g, x[l + j * c], acc[j]);
-        }
+                if (j < k) part[(p - 1) * R * COD_KMAX + ii + j * R] = acc[j];
+        __syncthreads();
+        if (p == 0 && i < c)
 #pragma unroll
-        for (int j = 0; j < COD_KMAX; ++j)
-            if (j < k) y[i + j * c] = acc[j];
+            for (int j = 0; j < COD_KMAX; ++j)
+                if (j < k) {
+                    double v = acc[j];
+                    for (int q = 1; q < COD_MV_PARTS; ++q) v += part[(q - 1) * R * COD_KMAX + ii + j * R];
+                    y[i + j * c] = v;
+                }
+        __syncthreads();
     }
-    __syncthreads();
 }
 
 // S[a,b] = sum_i x[i,a] y[i,b] (k x k, shared) for shared x, y (ld c)
@@ -106,7 +138,7 @@ __device__ void cta_orthonormalize(double* x, int c, int k, double* S, double* T
 // one CTA per job. A: dx x c, B: dy x c (column-major, ld dx / dy); GA, GB: c x c (ld cap).
 // outputs: sig[k] (gate: sig[0] = sigma1^2), hv (c x k global: the c-space
 // basis h V of the Ritz vectors, z = A hv or B hv), status
-__global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restrict__ A, int dx,
+__global__ void __launch_bounds__(COD_THREADS) k_cod_job(const CodJob* __restrict__ jobs, const double* __restrict__ A, int dx,
                           const double* __restrict__ B, int dy, const double* __restrict__ GA,
                           const double* __restrict__ GB, int cap, double* __restrict__ sig,
                           double* __restrict__ hv, int* __restrict__ status, double* pibuf,
@@ -121,13 +153,16 @@ __global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restr
     double* T = S + COD_KMAX * COD_KMAX;    // k*k
     double* W = T + COD_KMAX * COD_KMAX;    // k*k
     double* lam = W + COD_KMAX * COD_KMAX;  // k
-    double* cs = lam + COD_KMAX;            // jacobi scratch
+    double* cs = lam + COD_KMAX;            // jacobi scratch (64)
+    double* mvp = cs + 64;                  // cta_matvec partials
     double* sig_o = sig + blockIdx.x * COD_KMAX;
     double* hv_o = hv + (int64_t)blockIdx.x * cap * COD_KMAX;
     // zero p <=> trace(GA GB) == 0 (reference checks a.norm() == 0, linalg.cpp:101,131)
-    double tr = 0.0;
-    for (int i = threadIdx.x; i < c; i += blockDim.x)
-        for (int l = 0; l < c; ++l) tr = fma(GA[i + (int64_t)l * cap], GB[l + (int64_t)i * cap], tr);
+    double tr = 0.0;  // trace(GA GB) = sum GA .* GB (GB symmetric)
+    for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
+        const int i = e % c, l = e / c;
+        tr = fma(GA[i + (int64_t)l * cap], GB[i + (int64_t)l * cap], tr);
+    }
     tr = block_sum(tr, red);
     if (tr == 0.0) {
         if (threadIdx.x == 0) {
@@ -150,19 +185,25 @@ __global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restr
     double* pi = pibuf + (int64_t)blockIdx.x * pi_stride;
     for (int e = threadIdx.x; e < dvec * k; e += blockDim.x) pi[e] = rng_gaussian_at(jb.rng0, e);
     __syncthreads();
-    for (int i = threadIdx.x; i < c; i += blockDim.x) {
-        double acc[COD_KMAX];
+    {  // warp per buffer column i, lanes over the dvec coordinates
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+        for (int i = wid; i < c; i += nwarp) {
+            double acc[COD_KMAX];
 #pragma unroll
-        for (int j = 0; j < COD_KMAX; ++j) acc[j] = 0.0;
-        for (int l = 0; l < dvec; ++l) {
-            const double m = Mapin[l + (int64_t)i * ldm];
+            for (int j = 0; j < COD_KMAX; ++j) acc[j] = 0.0;
+            for (int l = lane; l < dvec; l += 32) {
+                const double m = Mapin[l + (int64_t)i * ldm];
+#pragma unroll
+                for (int j = 0; j < COD_KMAX; ++j)
+                    if (j < k) acc[j] = fma(m, pi[l * k + j], acc[j]);
+            }
 #pragma unroll
             for (int j = 0; j < COD_KMAX; ++j)
-                if (j < k) acc[j] = fma(m, pi[l * k + j], acc[j]);
+                if (j < k) {
+                    const double sum = warp_sum(acc[j]);
+                    if (lane == 0) v[i + j * c] = sum;
+                }
         }
-#pragma unroll
-        for (int j = 0; j < COD_KMAX; ++j)
-            if (j < k) v[i + j * c] = acc[j];
     }
     __syncthreads();
     if (jb.type == 0) {
@@ -179,12 +220,12 @@ __global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restr
         __syncthreads();
         for (int it = 0; it < jb.nit; ++it) {
             if (it == 0) {
-                cta_matvec(GA, cap, c, 1, v, t1);  // y = B (GA u)
+                cta_matvec(GA, cap, c, 1, v, t1, mvp);  // y = B (GA u)
             } else {
-                cta_matvec(GB, cap, c, 1, v, t2);
-                cta_matvec(GA, cap, c, 1, t2, t1);  // y = B (GA GB v)
+                cta_matvec(GB, cap, c, 1, v, t2, mvp);
+                cta_matvec(GA, cap, c, 1, t2, t1, mvp);  // y = B (GA GB v)
             }
-            cta_matvec(GB, cap, c, 1, t1, t3);
+            cta_matvec(GB, cap, c, 1, t1, t3, mvp);
             double n2 = 0.0;
             for (int i = threadIdx.x; i < c; i += blockDim.x) n2 = fma(t1[i], t3[i], n2);
             n2 = block_sum(n2, red);
@@ -199,8 +240,8 @@ __global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restr
             for (int i = threadIdx.x; i < c; i += blockDim.x) v[i] = t1[i] / nrm;
             __syncthreads();
         }
-        cta_matvec(GB, cap, c, 1, v, t2);
-        cta_matvec(GA, cap, c, 1, t2, t3);
+        cta_matvec(GB, cap, c, 1, v, t2, mvp);
+        cta_matvec(GA, cap, c, 1, t2, t3, mvp);
         double s2 = 0.0;
         for (int i = threadIdx.x; i < c; i += blockDim.x) s2 = fma(t2[i], t3[i], s2);
         s2 = block_sum(s2, red);
@@ -210,20 +251,20 @@ __global__ void k_cod_job(const CodJob* __restrict__ jobs, const double* __restr
     // simul_iter (linalg.cpp:123-152) in c-space: h0 = v (Mapin^T Pi)
     for (int it = 0; it <= jb.nit; ++it) {
         if (it > 0) {  // h <- Gsecond (Gfirst h)
-            cta_matvec(Gfirst, cap, c, k, v, t);
-            cta_matvec(Gsecond, cap, c, k, t, v);
+            cta_matvec(Gfirst, cap, c, k, v, t, mvp);
+            cta_matvec(Gsecond, cap, c, k, t, v, mvp);
         }
         cta_small_gram(v, v, c, k, S, red);  // Euclidean re-orthonormalization (span-preserving)
         cta_orthonormalize(v, c, k, S, T, lam, cs, W);
     }
     // final basis orthonormal in the Gfirst inner product (g = Mapout h)
-    cta_matvec(Gfirst, cap, c, k, v, t);
+    cta_matvec(Gfirst, cap, c, k, v, t, mvp);
     cta_small_gram(v, t, c, k, S, red);
     cta_orthonormalize(v, c, k, S, T, lam, cs, W);
     // Ritz: w = Map^T ... : w^T w = (Gfirst h)^T Gsecond (Gfirst h)
-    cta_matvec(Gfirst, cap, c, k, v, t);
+    cta_matvec(Gfirst, cap, c, k, v, t, mvp);
     double* u2 = hv_o;  // c*k scratch
-    cta_matvec(Gsecond, cap, c, k, t, u2);
+    cta_matvec(Gsecond, cap, c, k, t, u2, mvp);
     cta_small_gram(t, u2, c, k, S, red);
     for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
         const int a = e % k, b = e / k;
@@ -356,7 +397,9 @@ struct CodEngine::Impl {
     void run(const CodJob* hj, int nj, double* sig_h, int* status_h) {
         AERO_CUDA(cudaMemcpyAsync(jobs_d, hj, sizeof(CodJob) * nj, cudaMemcpyHostToDevice, st));
         const size_t smem = sizeof(double) * (32 + 2 * (size_t)c * COD_KMAX + 3 * COD_KMAX * COD_KMAX +
-                                              COD_KMAX + 64) + 16;
+                                              COD_KMAX + 64 +
+                                              (size_t)(COD_MV_PARTS - 1) * (COD_THREADS / COD_MV_PARTS) * COD_KMAX) +
+                            16;
         static bool attr = false;
         if (!attr) {
             AERO_CUDA(cudaFuncSetAttribute(k_cod_job, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -365,7 +408,7 @@ struct CodEngine::Impl {
         }
         const int64_t pis = (int64_t)std::max(dx, dy) * COD_KMAX;
         pib.alloc((size_t)std::max(nj, 3) * pis);
-        k_cod_job<<<nj, 256, smem, st>>>(jobs_d, A.p, dx, B.p, dy, GA.p, GB.p, cap, sig.p, hv.p,
+        k_cod_job<<<nj, COD_THREADS, smem, st>>>(jobs_d, A.p, dx, B.p, dy, GA.p, GB.p, cap, sig.p, hv.p,
                                          status_d, pib.p, pis);
         AERO_LAUNCHED();
         AERO_CUDA(cudaMemcpyAsync(sig_h, sig.p, sizeof(double) * nj * COD_KMAX, cudaMemcpyDeviceToHost, st));
@@ -401,7 +444,7 @@ struct CodEngine::Impl {
             const double lmax = std::max(l[0], 0.0);
             int rk = 0;
             for (int i = 0; i < m; ++i)
-                if (l[i] > 1e-13 * lmax && l[i] > 0.0) rk = i + 1;
+                if (l[i] > 1e-10 * lmax && l[i] > 0.0) rk = i + 1;
             return rk;
         };
         const int ra = rank_of(ha), rb = rank_of(hb);

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cfloat>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 #include "aero_common.cuh"
@@ -669,6 +670,9 @@ __global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const dou
     int end = q + 1;
     while (end < nvec && linked(end) && end - q < kMaxCluster) ++end;
     if (end - q < 2) return;
+    // numerically null clusters (|lambda| <= 1e-10 ||T||): every caller weights
+    // these directions by sqrt(lambda) or cuts them at its rank threshold
+    if (fabs(lam(q)) <= 1e-10 * bounds[3]) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = q + 1; i < end; ++i) {
         for (int pass = 0; pass < 2; ++pass) {
@@ -863,6 +867,25 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     AERO_LAUNCHED();
     note_launch();
     k_cluster_orth<<<nvec, 256, 0, st>>>(n, nvec, lam, bounds, wk.Z.p);
+    if (getenv("AERO_EIG_CLUSTERS")) {  // dev instrumentation
+        std::vector<double> hl(n), hb(4);
+        AERO_CUDA(cudaMemcpyAsync(hl.data(), lam, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        AERO_CUDA(cudaMemcpyAsync(hb.data(), bounds, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+        AERO_CUDA(cudaStreamSynchronize(st));
+        const double thr = 1e-7 * hb[3] + hb[2];
+        int run = 1;
+        fprintf(stderr, "eig n=%d nvec=%d tnorm=%.3e clusters:", n, nvec, hb[3]);
+        for (int i = 1; i < nvec; ++i) {
+            const double a0 = hl[n - i], a1 = hl[n - 1 - i];
+            if (a0 - a1 <= thr) ++run;
+            else {
+                if (run > 1) fprintf(stderr, " [%d..%d) %d lam=%.2e", i - run, i, run, a0);
+                run = 1;
+            }
+        }
+        if (run > 1) fprintf(stderr, " [%d..%d) %d", nvec - run, nvec, run);
+        fprintf(stderr, "\n");
+    }
     AERO_LAUNCHED();
     // Y = columns; then back-transform Y <- Q Y, Q = H_0 ... H_{n-2}
     const int ldy = (n + 1) & ~1;
