@@ -488,75 +488,21 @@ __global__ void __launch_bounds__(512, 1) k_sytrd_small(int n, const double* __r
     if (tid == 0) d[n - 1] = sa[(n - 1) + (n - 1) * n];
 }
 
-// Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x
-__device__ __forceinline__ int sturm_count(int n, const double* d, const double* e2, double x,
-                                           double pivmin) {
-    int cnt = 0;
-    double q = d[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
-    for (int i = 1; i < n; ++i) {
-        q = d[i] - x - e2[i - 1] / q;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
-    }
-    return cnt;
-}
-
-// one warp per eigenvalue index k (ascending, k >= k_lo): 33-way multisection
-// of the Gershgorin interval; d and e^2 staged in shared memory
-__global__ void k_bisect(int n, int k_lo, const double* __restrict__ d, const double* __restrict__ e2,
-                         const double* __restrict__ bounds, double* __restrict__ lam_asc) {
-    extern __shared__ double sde[];
-    double* sd = sde;
-    double* se = sde + n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        sd[i] = d[i];
-        se[i] = (i < n - 1) ? e2[i] : 0.0;
-    }
-    __syncthreads();
-    const int k = k_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (k >= n) return;
-    const double pivmin = bounds[2];
-    double lo = bounds[0], hi = bounds[1];
-    for (int round = 0; round < 64; ++round) {
-        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
-        if (hi - lo <= tol) break;
-        const double h = (hi - lo) / 33.0;
-        const double x = fmin(lo + h * (lane + 1), hi);
-        const int c = sturm_count(n, sd, se, x, pivmin);
-        const unsigned above = __ballot_sync(0xffffffffu, c > k);
-        double nlo = lo, nhi = hi;
-        if (above) {
-            const int f = __ffs(above) - 1;
-            nhi = __shfl_sync(0xffffffffu, x, f);
-            const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
-            if (f > 0) nlo = xp;
-        } else {
-            nlo = __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (nlo == lo && nhi == hi) break;  // interval can no longer be split
-        lo = nlo;
-        hi = nhi;
-    }
-    if (lane == 0) lam_asc[k] = 0.5 * (lo + hi);
-}
-
-// Gershgorin interval, pivmin, ||T||, e^2 (one CTA)
-__global__ void k_tri_prep(int n, const double* __restrict__ d, const double* __restrict__ e,
-                           double* __restrict__ e2, double* __restrict__ bounds) {
+// Gershgorin interval, pivmin, ||T||; T is split into unreduced blocks where
+// e_i^2 <= eps^2 |d_i d_{i+1}| + safmin or |e_i| <= eps ||T|| (LAPACK dstebz /
+// dsteqr criterion): e_i is set to 0 there. blk[i] = first row of i's block,
+// blk[n + i] = one past its last row. One CTA.
+__global__ void k_tri_prep(int n, const double* __restrict__ d, double* __restrict__ e,
+                           double* __restrict__ e2, double* __restrict__ bounds, int* __restrict__ blk) {
     __shared__ double smin[32], smax[32], se[32];
+    __shared__ double s_tnorm;
     double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double el = (i > 0) ? fabs(e[i - 1]) : 0.0;
         const double er = (i < n - 1) ? fabs(e[i]) : 0.0;
         lo = fmin(lo, d[i] - el - er);
         hi = fmax(hi, d[i] + el + er);
-        if (i < n - 1) {
-            e2[i] = e[i] * e[i];
-            emax = fmax(emax, e2[i]);
-        }
+        if (i < n - 1) emax = fmax(emax, e[i] * e[i]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -583,15 +529,114 @@ __global__ void k_tri_prep(int n, const double* __restrict__ d, const double* __
         bounds[1] = hi + pad;
         bounds[2] = pivmin;
         bounds[3] = tnorm;
+        s_tnorm = tnorm;
+    }
+    __syncthreads();
+    const double tnorm = s_tnorm;
+    for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
+        const double ei = e[i];
+        const bool split = ei * ei <= DBL_EPSILON * DBL_EPSILON * fabs(d[i] * d[i + 1]) + DBL_MIN ||
+                           fabs(ei) <= (double)n * DBL_EPSILON * tnorm;
+        if (split) e[i] = 0.0;
+        e2[i] = split ? 0.0 : ei * ei;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // block boundaries (sequential scan, n <= 4096)
+        int st = 0;
+        for (int i = 0; i < n; ++i) {
+            blk[i] = st;
+            if (i == n - 1 || e[i] == 0.0) {
+                for (int k = st; k <= i; ++k) blk[n + k] = i + 1;
+                st = i + 1;
+            }
+        }
     }
 }
 
-// eigenvector of T for lam (descending index q) by a twisted factorization.
-// Scratch Dp and output Z are row-interleaved: element i of vector q at
-// [i * nvec + q] so consecutive threads touch consecutive addresses.
+// Sturm count over rows [s, t): eigenvalues of that block strictly below x
+__device__ __forceinline__ int sturm_count(int s, int t, const double* d, const double* e2, double x,
+                                           double pivmin) {
+    int cnt = 0;
+    double q = d[s] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = s + 1; i < t; ++i) {
+        q = d[i] - x - e2[i - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
+// one warp per row p: the (p - s)-th smallest eigenvalue of p's block [s, t),
+// by 33-way multisection of the Gershgorin interval; d, e^2 in shared memory
+__global__ void k_bisect(int n, const double* __restrict__ d, const double* __restrict__ e2,
+                         const double* __restrict__ bounds, const int* __restrict__ blk,
+                         double* __restrict__ lam) {
+    extern __shared__ double sde[];
+    double* sd = sde;
+    double* se = sde + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sd[i] = d[i];
+        se[i] = (i < n - 1) ? e2[i] : 0.0;
+    }
+    __syncthreads();
+    const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n) return;
+    const int bs = blk[p], bt = blk[n + p], k = p - bs;
+    if (bt - bs == 1) {
+        if (lane == 0) lam[p] = sd[p];
+        return;
+    }
+    const double pivmin = bounds[2];
+    double lo = bounds[0], hi = bounds[1];
+    for (int round = 0; round < 64; ++round) {
+        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
+        if (hi - lo <= tol) break;
+        const double h = (hi - lo) / 33.0;
+        const double x = fmin(lo + h * (lane + 1), hi);
+        const int c = sturm_count(bs, bt, sd, se, x, pivmin);
+        const unsigned above = __ballot_sync(0xffffffffu, c > k);
+        double nlo = lo, nhi = hi;
+        if (above) {
+            const int f = __ffs(above) - 1;
+            nhi = __shfl_sync(0xffffffffu, x, f);
+            const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+            if (f > 0) nlo = xp;
+        } else {
+            nlo = __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (nlo == lo && nhi == hi) break;  // interval can no longer be split
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) lam[p] = 0.5 * (lo + hi);
+}
+
+// descending order of all eigenvalues (ties by row): order[q] = row, w[q] = lambda
+__global__ void k_order(int n, const double* __restrict__ lam, int* __restrict__ order, double* __restrict__ w) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double lp = lam[p];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+        const double li = lam[i];
+        rank += (li > lp) || (li == lp && i < p);
+    }
+    order[rank] = p;
+    w[rank] = lp;
+}
+
+// eigenvector (descending index q) of its unreduced block [s, t) by a twisted
+// factorization; zero outside the block. Scratch Dp and output Z are
+// row-interleaved: element i of vector q at [i * nvec + q], so consecutive
+// threads touch consecutive addresses.
 __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const double* __restrict__ e,
-                          const double* __restrict__ lam_asc, const double* __restrict__ bounds,
-                          double* __restrict__ Dp, double* __restrict__ Z) {
+                          const double* __restrict__ lam, const double* __restrict__ wdesc,
+                          const int* __restrict__ order, const int* __restrict__ blk,
+                          const double* __restrict__ bounds, double* __restrict__ Dp, double* __restrict__ L1,
+                          double* __restrict__ L2, double* __restrict__ L3, double* __restrict__ Z) {
     extern __shared__ double sde[];
     double* sd = sde;
     double* se = sde + n;
@@ -602,27 +647,120 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     __syncthreads();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nvec) return;
-    const double lam = lam_asc[n - 1 - q];
+    const int p = order[q];
+    const int bs = blk[p], bt = blk[n + p];
+    const double lv = lam[p];
     const double pivmin = bounds[2];
     auto safe = [&](double x) { return (fabs(x) < pivmin) ? -pivmin : x; };
+    for (int i = 0; i < bs; ++i) Z[(int64_t)i * nvec + q] = 0.0;
+    for (int i = bt; i < n; ++i) Z[(int64_t)i * nvec + q] = 0.0;
+    if (bt - bs == 1) {
+        Z[(int64_t)bs * nvec + q] = 1.0;
+        return;
+    }
     // top-down stationary qd: D+(i)
-    double dp = safe(sd[0] - lam);
-    Dp[q] = dp;
-    for (int i = 0; i < n - 1; ++i) {
-        dp = safe(sd[i + 1] - lam - se[i] * (se[i] / dp));
+    double dp = safe(sd[bs] - lv);
+    Dp[(int64_t)bs * nvec + q] = dp;
+    for (int i = bs; i < bt - 1; ++i) {
+        dp = safe(sd[i + 1] - lv - se[i] * (se[i] / dp));
         Dp[(int64_t)(i + 1) * nvec + q] = dp;
     }
+    // numerically repeated eigenvalue (gap to a neighbour < 1e-12 ||T||): a twisted
+    // vector is not determined; LAPACK dstein-style inverse iteration instead --
+    // shift perturbed below the earlier equal members of the block, pivoted LU
+    // (dlagtf / dlagts) in the interleaved scratch, pseudo-random start, two
+    // solves; k_cluster_orth then orthonormalizes the run
+    const double tdeg = 1e-12 * bounds[3];
+    const bool degen = (q > 0 && wdesc[q - 1] - wdesc[q] < tdeg) || (q + 1 < nvec && wdesc[q] - wdesc[q + 1] < tdeg);
+    if (degen) {
+        int cnt = 0;
+        for (int j = q - 1; j >= 0 && wdesc[j] - wdesc[q] < 1e-10 * bounds[3]; --j) cnt += blk[order[j]] == bs;
+        const double shift = lv - cnt * 10.0 * DBL_EPSILON * bounds[3];
+        const double tiny = DBL_EPSILON * bounds[3] + pivmin;
+        double* la = Dp;   // U diagonal
+        double* lb = L1;   // U first super-diagonal
+        double* ll = L2;   // multipliers, sign bit of L3 = pivot
+        double* ld2 = L3;  // U second super-diagonal
+        auto at = [&](double* a, int k) -> double& { return a[(int64_t)(bs + k) * nvec + q]; };
+        const int len = bt - bs;
+        for (int k = 0; k < len; ++k) {
+            at(la, k) = sd[bs + k] - shift;
+            at(lb, k) = (k < len - 1) ? se[bs + k] : 0.0;
+        }
+        // partial pivoting: |multiplier| <= 1, so a row swap is recorded as multiplier +- 4
+        for (int k = 0; k < len - 1; ++k) {
+            const double ck = se[bs + k];
+            double ak = at(la, k);
+            at(ld2, k) = 0.0;
+            if (fabs(ak) >= fabs(ck)) {
+                if (ak == 0.0) {
+                    ak = tiny;
+                    at(la, k) = tiny;
+                }
+                const double mult = ck / ak;
+                at(ll, k) = mult;
+                at(la, k + 1) -= mult * at(lb, k);
+            } else {
+                const double mult = ak / ck;
+                at(ll, k) = mult >= 0.0 ? mult + 4.0 : mult - 4.0;
+                at(la, k) = ck;
+                const double tmp = at(la, k + 1);
+                at(la, k + 1) = at(lb, k) - mult * tmp;
+                if (k < len - 2) {
+                    at(ld2, k) = at(lb, k + 1);
+                    at(lb, k + 1) = -mult * at(ld2, k);
+                }
+                at(lb, k) = tmp;
+            }
+        }
+        if (at(la, len - 1) == 0.0) at(la, len - 1) = tiny;
+        double nrm2 = 0.0;
+        for (int k = 0; k < len; ++k) {
+            uint64_t h = (uint64_t)(q + 1) * 0x9E3779B97F4A7C15ull ^ (uint64_t)(bs + k + 7) * 0xBF58476D1CE4E5B9ull;
+            h ^= h >> 31;
+            h *= 0x94D049BB133111EBull;
+            h ^= h >> 29;
+            const double v = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+            at(Z, k) = v;
+        }
+        for (int it = 0; it < 2; ++it) {
+            for (int k = 0; k < len - 1; ++k) {  // P L y = x
+                double m = at(ll, k);
+                const bool sw = fabs(m) > 2.0;
+                if (sw) m = m >= 0.0 ? m - 4.0 : m + 4.0;
+                const double xk = at(Z, k), xk1 = at(Z, k + 1);
+                if (!sw) {
+                    at(Z, k + 1) = xk1 - m * xk;
+                } else {
+                    at(Z, k) = xk1;
+                    at(Z, k + 1) = xk - m * xk1;
+                }
+            }
+            nrm2 = 0.0;
+            for (int k = len - 1; k >= 0; --k) {  // U z = y
+                double v = at(Z, k);
+                if (k < len - 1) v -= at(lb, k) * at(Z, k + 1);
+                if (k < len - 2) v -= at(ld2, k) * at(Z, k + 2);
+                v /= at(la, k);
+                at(Z, k) = v;
+                nrm2 += v * v;
+            }
+            const double sc = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+            for (int k = 0; k < len; ++k) at(Z, k) *= sc;
+        }
+        return;
+    }
     // bottom-up: D-(i) into Z, twist index by min |gamma|
-    double dm = safe(sd[n - 1] - lam);
-    Z[(int64_t)(n - 1) * nvec + q] = dm;
-    int r = n - 1;
-    double best = fabs(dp);  // gamma_{n-1} = D+(n-1)
+    double dm = safe(sd[bt - 1] - lv);
+    Z[(int64_t)(bt - 1) * nvec + q] = dm;
+    int r = bt - 1;
+    double best = fabs(dp);  // gamma at the last row = D+(last)
 #pragma unroll 4
-    for (int i = n - 2; i >= 0; --i) {
+    for (int i = bt - 2; i >= bs; --i) {
         const double dpi = Dp[(int64_t)i * nvec + q];
-        dm = safe(sd[i] - lam - se[i] * (se[i] / dm));
+        dm = safe(sd[i] - lv - se[i] * (se[i] / dm));
         Z[(int64_t)i * nvec + q] = dm;
-        const double g = dpi + dm - (sd[i] - lam);
+        const double g = dpi + dm - (sd[i] - lv);
         if (fabs(g) < best) {
             best = fabs(g);
             r = i;
@@ -631,7 +769,7 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     // solve outward from r
     double nrm2 = 1.0, z = 1.0;
 #pragma unroll 4
-    for (int i = r; i < n - 1; ++i) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
+    for (int i = r; i < bt - 1; ++i) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
         const double dmn = Z[(int64_t)(i + 1) * nvec + q];
         z = -(se[i] / dmn) * z;
         Z[(int64_t)(i + 1) * nvec + q] = z;
@@ -640,39 +778,48 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     Z[(int64_t)r * nvec + q] = 1.0;
     z = 1.0;
 #pragma unroll 4
-    for (int i = r - 1; i >= 0; --i) {  // z_i = -(e_i / D+(i)) z_{i+1}
+    for (int i = r - 1; i >= bs; --i) {  // z_i = -(e_i / D+(i)) z_{i+1}
         z = -(se[i] / Dp[(int64_t)i * nvec + q]) * z;
         Z[(int64_t)i * nvec + q] = z;
         nrm2 += z * z;
     }
-    const double s = 1.0 / sqrt(nrm2);
+    const double sc = 1.0 / sqrt(nrm2);
 #pragma unroll 4
-    for (int i = 0; i < n; ++i) Z[(int64_t)i * nvec + q] *= s;
+    for (int i = bs; i < bt; ++i) Z[(int64_t)i * nvec + q] *= sc;
 }
 
 // re-orthonormalize the vectors of each cluster of close eigenvalues
 // (classical Gram-Schmidt applied twice, one CTA per cluster leader; clusters
-// longer than kMaxCluster are cut into consecutive groups of that length)
+// longer than kMaxCluster are cut into consecutive groups of that length).
+// Vectors of different unreduced blocks have disjoint support (exactly
+// orthogonal); inside a block the eigenvalues are distinct.
 constexpr int kMaxCluster = 128;
-__global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const double* __restrict__ lam_asc,
+__global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const double* __restrict__ wdesc,
                                                       const double* __restrict__ bounds, double* __restrict__ Z) {
-    __shared__ double dots[kMaxCluster];
     __shared__ double red[64];
+    extern __shared__ double dots[];  // n
     const int q = blockIdx.x;
     const double thr = 1e-7 * bounds[3] + bounds[2];
-    auto lam = [&](int i) { return lam_asc[n - 1 - i]; };  // descending
-    auto linked = [&](int i) { return i > 0 && lam(i - 1) - lam(i) <= thr; };
-    if (linked(q)) {  // leader of a later group of a long cluster?
-        int st = q;
-        while (st > 0 && linked(st)) --st;
+    auto linked = [&](int i) { return i > 0 && wdesc[i - 1] - wdesc[i] <= thr; };
+    // the whole run of linked eigenvalues around q
+    int st = q;
+    while (st > 0 && linked(st)) --st;
+    int fend = st + 1;
+    while (fend < nvec && linked(fend)) ++fend;
+    bool degenerate = false;
+    for (int i = st + 1; i < fend; ++i) degenerate |= (wdesc[i - 1] - wdesc[i]) < 1e-12 * bounds[3];
+    int end;
+    if (degenerate) {  // one CTA handles the whole run (members made orthogonal to all earlier ones)
+        if (q != st) return;
+        end = fend;
+    } else {  // independent groups of at most kMaxCluster
         if ((q - st) % kMaxCluster != 0) return;
+        end = min(fend, q + kMaxCluster);
     }
-    int end = q + 1;
-    while (end < nvec && linked(end) && end - q < kMaxCluster) ++end;
     if (end - q < 2) return;
     // numerically null clusters (|lambda| <= 1e-10 ||T||): every caller weights
     // these directions by sqrt(lambda) or cuts them at its rank threshold
-    if (fabs(lam(q)) <= 1e-10 * bounds[3]) return;
+    if (fabs(wdesc[q]) <= 1e-10 * bounds[3]) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = q + 1; i < end; ++i) {
         for (int pass = 0; pass < 2; ++pass) {
@@ -743,14 +890,8 @@ __global__ void k_larft(int nref, const double* __restrict__ S, const double* __
     for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) Tb[idx] = sT[idx];
 }
 
-// eigenvalues descending into w (indices beyond the computed range: 0)
-__global__ void k_desc(int n, int k_lo, const double* __restrict__ lam_asc, double* __restrict__ w) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) w[i] = (n - 1 - i >= k_lo) ? lam_asc[n - 1 - i] : 0.0;
-}
-
 struct Work {
-    DeviceBuf V, W, vec, Z, Dp, Y, S, T, M1, M2, ws;
+    DeviceBuf V, W, vec, Z, Dp, L, Y, S, T, M1, M2, ws;
     unsigned* bar = nullptr;
     int grid = 0;
 };
@@ -788,6 +929,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
                                        (int)(2 * sizeof(double) * kEighLargeMax)));
         AERO_CUDA(cudaFuncSetAttribute(k_twisted, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(2 * sizeof(double) * kEighLargeMax)));
+        AERO_CUDA(cudaFuncSetAttribute(k_cluster_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * kEighLargeMax)));
         AERO_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * (BT_NB * BT_NB + BT_NB))));
         int sms = 0;
@@ -801,7 +944,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     const size_t n2 = (size_t)n * n;
     wk.V.alloc(n2);
     wk.W.alloc((size_t)n * TRD_NB);
-    wk.vec.alloc((size_t)9 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB + 8);
+    wk.vec.alloc((size_t)11 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB + 8);
     double* d = wk.vec.p;
     double* e = d + n;
     double* tau = e + n;
@@ -813,6 +956,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     double* slots = lam + n + n;
     double* dots = slots + SLOTW * wk.grid;
     double* bounds = dots + 2 * TRD_NB;
+    int* blk = reinterpret_cast<int*>(bounds + 8);       // 2n ints
+    int* order = blk + 2 * n;                            // n ints
     fill_zero(st, wk.V.p, (int64_t)n2);
     fill_zero(st, e, n);
     fill_zero(st, tau, n);
@@ -846,46 +991,26 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     }
 
     note_launch();
-    k_tri_prep<<<1, 1024, 0, st>>>(n, d, e, e2, bounds);
+    k_tri_prep<<<1, 1024, 0, st>>>(n, d, e, e2, bounds, blk);
     AERO_LAUNCHED();
-    // eigenvalues: all when every vector is wanted, else the top nvec + 1
-    const int k_lo = (nvec >= n) ? 0 : n - (nvec + 1);
-    const int nk = n - k_lo;
     const size_t sde = 2 * sizeof(double) * (size_t)n;
     note_launch();
-    k_bisect<<<(nk * 32 + 127) / 128, 128, sde, st>>>(n, k_lo, d, e2, bounds, lam);
+    k_bisect<<<(n * 32 + 127) / 128, 128, sde, st>>>(n, d, e2, bounds, blk, lam);
     AERO_LAUNCHED();
     note_launch();
-    k_desc<<<(n + 255) / 256, 256, 0, st>>>(n, k_lo, lam, w);
+    k_order<<<(n + 127) / 128, 128, 0, st>>>(n, lam, order, w);
     AERO_LAUNCHED();
 
     // eigenvectors of T for the top nvec eigenvalues
     wk.Dp.alloc((size_t)n * nvec);
     wk.Z.alloc((size_t)n * nvec);
     note_launch();
-    k_twisted<<<(nvec + 31) / 32, 32, sde, st>>>(n, nvec, d, e, lam, bounds, wk.Dp.p, wk.Z.p);
+    wk.L.alloc((size_t)3 * n * nvec);
+    k_twisted<<<(nvec + 31) / 32, 32, sde, st>>>(n, nvec, d, e, lam, w, order, blk, bounds, wk.Dp.p, wk.L.p,
+                                                 wk.L.p + (size_t)n * nvec, wk.L.p + (size_t)2 * n * nvec, wk.Z.p);
     AERO_LAUNCHED();
     note_launch();
-    k_cluster_orth<<<nvec, 256, 0, st>>>(n, nvec, lam, bounds, wk.Z.p);
-    if (getenv("AERO_EIG_CLUSTERS")) {  // dev instrumentation
-        std::vector<double> hl(n), hb(4);
-        AERO_CUDA(cudaMemcpyAsync(hl.data(), lam, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-        AERO_CUDA(cudaMemcpyAsync(hb.data(), bounds, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
-        AERO_CUDA(cudaStreamSynchronize(st));
-        const double thr = 1e-7 * hb[3] + hb[2];
-        int run = 1;
-        fprintf(stderr, "eig n=%d nvec=%d tnorm=%.3e clusters:", n, nvec, hb[3]);
-        for (int i = 1; i < nvec; ++i) {
-            const double a0 = hl[n - i], a1 = hl[n - 1 - i];
-            if (a0 - a1 <= thr) ++run;
-            else {
-                if (run > 1) fprintf(stderr, " [%d..%d) %d lam=%.2e", i - run, i, run, a0);
-                run = 1;
-            }
-        }
-        if (run > 1) fprintf(stderr, " [%d..%d) %d", nvec - run, nvec, run);
-        fprintf(stderr, "\n");
-    }
+    k_cluster_orth<<<nvec, 256, sizeof(double) * (size_t)n, st>>>(n, nvec, w, bounds, wk.Z.p);
     AERO_LAUNCHED();
     // Y = columns; then back-transform Y <- Q Y, Q = H_0 ... H_{n-2}
     const int ldy = (n + 1) & ~1;

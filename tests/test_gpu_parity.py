@@ -281,6 +281,22 @@ def test_eigh_matches_oracle(orc, n):
     assert np.max(np.abs(v[:, sep] - vr[:, sep])) < 1e-8
 
 
+@pytest.mark.parametrize("n", [64, 200, 512])
+def test_eigh_repeated_eigenvalues(orc, n):
+    """Exactly repeated eigenvalues in a non-axis basis (the tridiagonal form then
+    splits or holds numerically equal eigenvalues): eigenvectors must still form
+    an orthonormal eigenbasis; the identity is the fully split extreme."""
+    a = gaussian(orc, n, n, 13, n)
+    q, _ = np.linalg.qr(a)
+    lam = np.concatenate([np.full(n // 4, 5.0), np.full(n // 2, 3.0), np.linspace(1.0, 2.0, n - n // 4 - n // 2)])
+    for b in ((q * lam) @ q.T, 2.0 * np.eye(n)):
+        w, v = prod.eigh(b)
+        assert np.all(np.isfinite(v))
+        assert np.max(np.abs(np.sort(w) - np.sort(np.linalg.eigvalsh(b)))) <= 1e-12 * 5.0
+        assert np.linalg.norm(v @ np.diag(w) @ v.T - b) <= 1e-12 * np.linalg.norm(b)
+        assert np.linalg.norm(v.T @ v - np.eye(n)) < 1e-11
+
+
 @pytest.mark.parametrize("n,rank", [(256, 100), (512, 511), (600, 40)])
 def test_eigh_rank_deficient_gram(orc, n, rank):
     """FD-reduce-shaped input: a Gram matrix with an exact null space (clusters
