@@ -235,6 +235,34 @@ def run_other(args, cfg, world, rank, local):
     nrows = S * (steps + warm)
     kind = cfg["kind"]
     ts_all = np.arange(1, nrows + 1, dtype=np.int64)
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(upd):
+        """W warm-up steps, then K steps bracketed by barrier + CUDA events on the
+        current stream (every update_block returns after its own streams finished)."""
+        for w in range(warm):
+            upd(slice(w * S, (w + 1) * S))
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = prod.kernel_launches()
+        with ClockSampler(local) as clk:
+            e0.record()
+            for k in range(warm, warm + steps):
+                upd(slice(k * S, (k + 1) * S))
+            e1.record()
+            e1.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, int(prod.kernel_launches() - l0), clk.summary()
+
+    extra = {}
     if kind == "amm":
         g = torch.Generator(device=dev).manual_seed(1)
         W = torch.randn((cfg["latent"], cfg["dx"] + cfg["dy"]), generator=g, device=dev, dtype=torch.float64)
@@ -245,53 +273,51 @@ def run_other(args, cfg, world, rank, local):
         for t in (x, y):  # squared norms log-uniform on (1, R]
             u = torch.rand((nrows, 1), generator=g, device=dev, dtype=torch.float64)
             t.mul_(torch.sqrt(cfg["r_max"] ** u / (t * t).sum(1, keepdim=True)))
-        x, y = x.cpu().numpy(), y.cpu().numpy()
+        x, y = x.cpu().pin_memory().numpy(), y.cpu().pin_memory().numpy()
         state = prod.CodState(cfg["dx"], cfg["dy"], cfg["eps"], cfg["eps"] * cfg["window"], cfg["window"],
                               seed=1, stream=1000, device=local)
-        upd = lambda sl: state.update_block(x[sl], y[sl], ts_all[sl])  # noqa: E731
+        ms, launches, clocks = timed(lambda sl: state.update_block(x[sl], y[sl], ts_all[sl]))
         unit_rows = 1
+        # the CodState API (amm.hpp:35-69) takes host rows: the only path is host -> device
+        e2e = {"value": S * steps / (ms * 1e-3), "unit": "rows/s", "h2d_bytes_per_step": S * (cfg["dx"] + cfg["dy"]) * 8,
+               "d2h_bytes_per_step": S * 64}
+        extra["value_path"] = "host rows through the public API (CodState has no device-pointer entry point)"
     else:
         rows = torch.empty((nrows, cfg["d"]), dtype=torch.float64, device=dev)
         prod.gen_rows_device(rows, 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1,
                              stream=rank, drift=cfg.get("drift", 0), k2=cfg.get("k2", 0),
                              rho2=cfg.get("rho2", 0.9), scale2=cfg.get("scale2", 0.5), device=local)
         torch.cuda.synchronize(dev)
+        host = rows.cpu().pin_memory().numpy()
         if kind == "sw":
-            state = prod.MlState(cfg["d"], cfg["window"], cfg["r_max"], cfg["eps"], seed=1, stream=1000,
-                                 device=local)
-            upd = lambda sl: state.update_block(rows[sl], ts_all[sl])  # noqa: E731
+            def make():
+                return prod.MlState(cfg["d"], cfg["window"], cfg["r_max"], cfg["eps"], seed=1, stream=1000,
+                                    device=local)
+            st1 = make()
+            ms, launches, clocks = timed(lambda sl: st1.update_block(rows[sl], ts_all[sl]))
+            del st1
+            st2 = make()
+            ms2, _, _ = timed(lambda sl: st2.update_block(host[sl], ts_all[sl]))
+            del st2
             unit_rows = 1
         else:  # dist: sites j == rank (m = world)
             from paper_2601_02019_b200.distributed import DistributedSketch
-            state = DistributedSketch(cfg["d"], cfg["eps"], world, seed=1, rank=rank, world=world,
-                                      group=group, device=local, use_nccl=world > 1)
-            upd = lambda sl: state.ingest({rank: rows[sl]}, sl.start + 1)  # noqa: E731
+
+            def make():
+                return DistributedSketch(cfg["d"], cfg["eps"], world, seed=1, rank=rank, world=world,
+                                         group=group, device=local, use_nccl=world > 1)
+            st1 = make()
+            ms, launches, clocks = timed(lambda sl: st1.ingest({rank: rows[sl]}, sl.start + 1))
+            sk, _ = st1.probe()  # NCCL merge (outside the timed region, like the reference's probes)
+            extra["probe_ok"] = bool(np.isfinite(sk).all())
+            del st1
+            st2 = make()
+            ms2, _, _ = timed(lambda sl: st2.ingest({rank: host[sl]}, sl.start + 1))
+            del st2
             unit_rows = world
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize(dev)
-
-    for w in range(warm):
-        upd(slice(w * S, (w + 1) * S))
-    barrier()
-    l0 = prod.kernel_launches()
-    with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
-        for k in range(warm, warm + steps):
-            upd(slice(k * S, (k + 1) * S))
-        barrier()
-        dt = time.perf_counter() - t0  # every update_block returns after its stream synchronized
-    if world > 1:
-        t = torch.tensor([dt], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dt = float(t.item())
-    value = unit_rows * S * steps / dt
-    extra = {}
-    if kind == "dist":
-        sk, _ = state.probe()  # NCCL merge (outside the timed region, like the reference's probes)
-        extra["probe_ok"] = bool(np.isfinite(sk).all())
+        e2e = {"value": unit_rows * S * steps / (ms2 * 1e-3), "unit": "row-site updates/s" if kind == "dist" else "rows/s",
+               "h2d_bytes_per_step": S * cfg["d"] * 8, "d2h_bytes_per_step": 0}
+    value = unit_rows * S * steps / (ms * 1e-3)
     if rank == 0:
         cpu = None
         if not args.no_cpu:
@@ -301,13 +327,12 @@ def run_other(args, cfg, world, rank, local):
         print(json.dumps({
             "metric": "sketch update throughput", "value": value,
             "unit": "row-site updates/s" if kind == "dist" else "rows/s", "n_gpus": world, "steps": steps,
-            "warmup": warm, "ms_per_step": dt * 1e3 / steps, "higher_is_better": True,
+            "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "rows_per_step": S, "timed_rows": f"{warm * S + 1}..{nrows}",
-                       "parallelism": f"sites={world}" if kind == "dist" else "single",
-                       "timing": "host wall clock around blocking update_block calls (device work completes inside)"},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(prod.kernel_launches() - l0),
-            "clocks": clk.summary(), **extra}), flush=True)
+                       "parallelism": f"sites={world}" if kind == "dist" else "single"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, **extra}), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -375,11 +400,11 @@ def main():
             ms = float(t.item())
         return ms, launches, clk.summary(), np.concatenate(evs)
 
-    sk = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, profile=True)
+    sk = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local)
     ms, launches, clocks, ev = run(sk)
-    prof = sk.profile()
     info = sk.info()
     value = world * S * steps / (ms * 1e-3)
+    del sk
 
     e2e = None
     if not args.no_e2e:
@@ -389,6 +414,14 @@ def main():
         e2e = {"value": world * S * steps / (ms2 * 1e-3), "unit": "rows/s",
                "h2d_bytes_per_step": S * d * 8, "d2h_bytes_per_step": S * ev.dtype.itemsize}
         del sk2, host
+
+    # roofline counters: a third, profiled pass over the same rows (per-launch
+    # CUDA events around the product kernels slow the step, so `value` above
+    # comes from the unprofiled pass)
+    skp = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, profile=True)
+    ms_p, _, _, _ = run(skp)
+    prof = skp.profile()
+    del skp
 
     out = None
     if rank == 0:
@@ -403,9 +436,9 @@ def main():
                 traffic = None
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
-                    "kernel": "k_dgemm (batched masked G.X power/subspace-iteration product)",
+                    "kernel": "k_product (batched masked G.X power/subspace-iteration product, product.cu)",
                     "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 fp64 (not in MEASURED_PEAKS.json)",
-                    "product_share_of_step": prof["product_ms"] / ms,
+                    "product_share_of_step": prof["product_ms"] / ms_p,
                     "flops_per_launch": prof["product_flops"] / max(1, prof["product_launches"]),
                     "ms_per_launch": prof["product_ms"] / max(1, prof["product_launches"])}
         cpu = None
