@@ -2,6 +2,7 @@
 #include <cublas_v2.h>
 #include <cstdio>
 #include <vector>
+#include <cmath>
 #include "../paper_2601_02019_b200/csrc/kernels.cuh"
 using namespace aero_b200;
 int main() {
@@ -40,8 +41,24 @@ int main() {
                 cudaEventElapsedTime(&ms, e0, e1);
                 bestc = ms < bestc ? ms : bestc;
             }
-            printf("R=%4d N=%3d  ours %7.1f us %6.2f TF/s   cublas %7.1f us %6.2f TF/s\n", R, N,
-                   best * 1e3, fl / (best * 1e-3) / 1e12, bestc * 1e3, fl / (bestc * 1e-3) / 1e12);
+            // correctness vs cuBLAS
+            double *Y2;
+            cudaMalloc(&Y2, sizeof(double) * cap * N);
+            gemm_product(0, R, N, R, G, cap, X, cap, Y2, cap, nullptr, ws, wsn);
+            const double one = 1.0, zero = 0.0;
+            cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, R, N, R, &one, G, cap, X, cap, &zero, Y, cap);
+            std::vector<double> h1((size_t)cap * N), h2((size_t)cap * N);
+            cudaMemcpy(h1.data(), Y, sizeof(double) * cap * N, cudaMemcpyDeviceToHost);
+            cudaMemcpy(h2.data(), Y2, sizeof(double) * cap * N, cudaMemcpyDeviceToHost);
+            double md = 0, mx = 0;
+            for (int j = 0; j < N; ++j)
+                for (int i = 0; i < R; ++i) {
+                    md = fmax(md, fabs(h1[i + (size_t)j * cap] - h2[i + (size_t)j * cap]));
+                    mx = fmax(mx, fabs(h1[i + (size_t)j * cap]));
+                }
+            cudaFree(Y2);
+            printf("R=%4d N=%3d  ours %7.1f us %6.2f TF/s   cublas %7.1f us %6.2f TF/s  relmax %.1e\n", R, N,
+                   best * 1e3, fl / (best * 1e-3) / 1e12, bestc * 1e3, fl / (bestc * 1e-3) / 1e12, md / mx);
         }
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
