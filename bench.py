@@ -436,7 +436,7 @@ def main():
                 traffic = None
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak if peak > 0 else None, "traffic": traffic,
-                    "kernel": "k_product (batched masked G.X power/subspace-iteration product, product.cu)",
+                    "kernel": "k_iterate (persistent: split-K DMMA G.X products of every phase of a batch + per-job normalization, kernels.cu); useful product flops over the whole kernel time",
                     "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 fp64 (not in MEASURED_PEAKS.json)",
                     "product_share_of_step": prof["product_ms"] / ms_p,
                     "flops_per_launch": prof["product_flops"] / max(1, prof["product_launches"]),

@@ -6,6 +6,7 @@
 
 #include "aero_common.cuh"
 #include "kernels.cuh"
+#include "tiles.cuh"
 
 namespace aero_b200 {
 
@@ -466,17 +467,22 @@ __device__ void small_eig(double* W, double* T, int k, double* cs) {
 
 // WS: Y arrives as `splits` split-K partials in ws (ws[z*sstride + i + c*wsM]),
 // summed here in fixed order into shared memory (fuses k_product_reduce)
+template <int KM>
+__host__ __device__ constexpr size_t normalize_smem_doubles(int R, bool ws) {
+    return 32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM) + (ws ? (size_t)R * KM : 0);
+}
+
+// one job's normalization after product phase `phase` (body of k_iter_normalize;
+// also run inside the persistent k_iterate); sm: normalize_smem_doubles
 template <int KM, bool WS>
-__global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, double* X,
-                                 const double* __restrict__ Y, int ldx, double* H,
-                                 int* __restrict__ status, double* __restrict__ out_sig,
-                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
-                                 const double* __restrict__ ws, int wsM, int64_t sstride,
-                                 int splits) {
-    extern __shared__ double sm[];
-    const IterJob jb = jobs[blockIdx.x];
+__device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
+                              const double* __restrict__ Y, int ldx, double* H,
+                              int* __restrict__ status, double* __restrict__ out_sig,
+                              double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
+                              const double* __restrict__ ws, int wsM, int64_t sstride, int splits,
+                              double* sm) {
     if (phase >= jb.nphase) return;
-    const int st = status[blockIdx.x];
+    const int st = status[jidx];
     const bool last = (phase == jb.nphase - 1);
     const int tid = threadIdx.x, nt = blockDim.x;
     const int r = jb.r, k = jb.k;
@@ -503,7 +509,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
             const int i = e % r, a = e / r;
             const double* p = ws + i + (int64_t)(jb.col + a) * wsM;
             double v = 0.0;
-            for (int z = 0; z < splits; ++z) v += p[z * sstride];
+            for (int z = 0; z < splits; ++z) v += __ldcg(p + z * sstride);
             ysh[e] = v;
         }
         __syncthreads();
@@ -520,7 +526,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
             s = block_sum(s, red);
             const double nrm = sqrt(s);
             if (nrm < 1e-300) {  // linalg.cpp:112-116
-                if (tid == 0) status[blockIdx.x] = JOB_DEAD;
+                if (tid == 0) status[jidx] = JOB_DEAD;
                 return;
             }
             for (int i = tid; i < r; i += nt) x[i] = y[i] / nrm;
@@ -551,7 +557,7 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
             lam[i] = ok ? 1.0 / sqrt(l) : 0.0;
             nclamp += !ok;
         }
-        if (last && out_clamped) out_clamped[blockIdx.x] = nclamp;
+        if (last && out_clamped) out_clamped[jidx] = nclamp;
     }
     __syncthreads();
     for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
@@ -597,12 +603,24 @@ __global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, do
 }
 
 template <int KM, bool WS>
+__global__ void k_iter_normalize(const IterJob* __restrict__ jobs, int phase, double* X,
+                                 const double* __restrict__ Y, int ldx, double* H,
+                                 int* __restrict__ status, double* __restrict__ out_sig,
+                                 double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
+                                 const double* __restrict__ ws, int wsM, int64_t sstride,
+                                 int splits) {
+    extern __shared__ double sm[];
+    const IterJob jb = jobs[blockIdx.x];
+    normalize_job<KM, WS>(jb, blockIdx.x, phase, X, Y, ldx, H, status, out_sig, out_vr, kv, out_clamped, ws,
+                          wsM, sstride, splits, sm);
+}
+
+template <int KM, bool WS>
 static void launch_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
                              const double* Y, int ldx, double* H, int* status, double* out_sig,
                              double* out_vr, int kv, int* out_clamped, const double* ws, int wsM,
                              int64_t sstride, int splits) {
-    const size_t smem = sizeof(double) * (32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM) +
-                                          (WS ? (size_t)wsM * KM : 0)) + 16;
+    const size_t smem = sizeof(double) * normalize_smem_doubles<KM>(wsM, WS) + 16;
     if (smem > 48 * 1024)
         AERO_CUDA(cudaFuncSetAttribute(k_iter_normalize<KM, WS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -610,6 +628,89 @@ static void launch_normalize(cudaStream_t st, const IterJob* jobs, int njobs, in
                                                        out_vr, kv, out_clamped, ws, wsM, sstride,
                                                        splits);
     AERO_LAUNCHED();
+}
+
+// ---- persistent iteration: every phase of a batch in ONE cooperative launch --
+// phase p: [all CTAs] split-K partial products Y_z = G[:, Kz] X[Kz, :] as DMMA
+// tiles -> grid barrier -> [CTA per job] fixed-order partial sum + normalize ->
+// grid barrier. Replaces (product + reduce + normalize) launches per phase.
+struct IterPersistArgs {
+    const IterJob* jobs;
+    int njobs, maxphase, R, ldg, ldx, kv;
+    const double* G;
+    double *X, *H, *out_sig, *out_vr, *ws;
+    int *status, *out_clamped;
+    const int* phase_ncol;    // active columns per phase
+    const int* phase_splits;  // split-K factor per phase
+    unsigned* bar;
+};
+
+template <int KM>
+__global__ void __launch_bounds__(tiles::PNT, 2) k_iterate(IterPersistArgs a) {
+    using namespace tiles;
+    extern __shared__ __align__(16) double smd[];
+    unsigned epoch = 0;
+    const unsigned G = gridDim.x;
+    const int R = a.R;
+    const int kt_total = (R + PBK - 1) / PBK;
+    for (int p = 0; p < a.maxphase; ++p) {
+        const int ncol = a.phase_ncol[p], splits = a.phase_splits[p];
+        const int tn = (ncol + PBN - 1) / PBN, tmn = (R + PBM - 1) / PBM;
+        const int kchunk = ((kt_total + splits - 1) / splits) * PBK;
+        const int items = tn * tmn * splits;
+        const int64_t sstride = (int64_t)R * ncol;
+        for (int it = blockIdx.x; it < items; it += G) {
+            const int tz = it / (tn * tmn), rem = it % (tn * tmn);
+            mma_tile<false, false>(rem % tn, rem / tn, tz, R, ncol, R, kchunk, a.G, a.ldg, a.X, a.ldx, a.ws, R,
+                                   sstride, nullptr, 0, 1.0, 0.0, smd);
+            __syncthreads();
+        }
+        grid_sync(a.bar, epoch, G);
+        for (int j = blockIdx.x; j < a.njobs; j += G) {
+            const IterJob jb = a.jobs[j];
+            normalize_job<KM, true>(jb, j, p, a.X, nullptr, a.ldx, a.H, a.status, a.out_sig, a.out_vr, a.kv,
+                                    a.out_clamped, a.ws, R, sstride, splits, smd);
+            __syncthreads();
+        }
+        grid_sync(a.bar, epoch, G);
+    }
+}
+
+size_t iterate_smem_bytes(int R) {
+    return std::max(tiles::MMA_SMEM, sizeof(double) * normalize_smem_doubles<4>(R, true)) + 16;
+}
+
+int iterate_grid(int R) {
+    static int grid[2] = {0, 0};
+    static int ok_r = -1;
+    if (ok_r != R) {
+        int dev = 0, sms = 0, per2 = 0, per4 = 0;
+        AERO_CUDA(cudaGetDevice(&dev));
+        AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const size_t smem = iterate_smem_bytes(R);
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AERO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_iterate<2>, tiles::PNT, smem));
+        AERO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per4, k_iterate<4>, tiles::PNT, smem));
+        grid[0] = sms * std::min(per2, 2);
+        grid[1] = sms * std::min(per4, 2);
+        ok_r = R;
+    }
+    return std::min(grid[0], grid[1]);
+}
+
+void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const double* G,
+                        int ldg, double* X, int ldx, double* H, int* status, double* out_sig, double* out_vr,
+                        int kv, int* out_clamped, double* ws, const int* phase_ncol, const int* phase_splits,
+                        unsigned* bar, int max_k) {
+    const int grid = iterate_grid(R);
+    AERO_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), st));
+    IterPersistArgs a{jobs, njobs, maxphase, R, ldg, ldx, kv, G, X, H, out_sig, out_vr, ws, status, out_clamped,
+                      phase_ncol, phase_splits, bar};
+    void* args[] = {&a};
+    note_launch();
+    AERO_CUDA(cudaLaunchCooperativeKernel(max_k <= 2 ? (void*)k_iterate<2> : (void*)k_iterate<4>, dim3(grid),
+                                          dim3(tiles::PNT), args, iterate_smem_bytes(R), st));
 }
 
 void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,

@@ -103,7 +103,7 @@ Sketch::Sketch(const aero_cfg& cfg) {
     X_.alloc((size_t)ldx_ * ncols_);
     Y_.alloc((size_t)ldx_ * ncols_);
     H_.alloc((size_t)ldx_ * ncols_);
-    ws_.alloc(product_workspace_doubles(cap_, ncols_));
+    ws_.alloc(product_workspace_doubles(cap_, std::max(ncols_, cap_ / 4)));  // split-K partials
     sig_.alloc(ncols_);
     vr_.alloc((size_t)ncols_ * kv_);
     small_.alloc(4 * 64 * 64 + 64);
@@ -112,6 +112,9 @@ Sketch::Sketch(const aero_cfg& cfg) {
     colmask_d_ = dev_alloc<int>(ncols_);
     jobs_d_ = dev_alloc<IterJob>(ncols_);
     jobs_h_ = pinned<IterJob>(ncols_);
+    phase_d_ = dev_alloc<int>(2 * kMaxPhases);
+    phase_h_ = pinned<int>(2 * kMaxPhases);
+    bar_d_ = dev_alloc<unsigned>(1);
     colmask_h_ = pinned<int>(ncols_);
     sig_h_ = pinned<double>(std::max(ncols_, cap_));
     status_h_ = pinned<int>(ncols_);
@@ -142,6 +145,9 @@ Sketch::~Sketch() {
         delete c;
     }
     cudaFree(status_d_);
+    cudaFree(phase_d_);
+    cudaFree(bar_d_);
+    cudaFreeHost(phase_h_);
     cudaFree(clamp_d_);
     cudaFree(colmask_d_);
     cudaFree(jobs_d_);
@@ -256,6 +262,42 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob) * njobs, cudaMemcpyHostToDevice, st_));
     AERO_CUDA(cudaMemcpyAsync(colmask_d_, colmask_h_, sizeof(int) * ncol_total,
                               cudaMemcpyHostToDevice, st_));
+    // persistent launch when the phases are launch-latency bound (small products);
+    // large products run as separate DMMA launches (measured faster there)
+    double big = 0.0;
+    for (int j = 0; j < njobs; ++j) big = std::max(big, (double)jobs_h_[j].r);
+    const bool small_phases = big * big * (double)ncol_total < 1e8;
+    if (max_k <= 4 && maxphase <= kMaxPhases && persistent_ && small_phases) {
+        // all phases in one cooperative launch (kernels.cu k_iterate)
+        const int grid = iterate_grid(R);
+        const int kt = (R + 15) / 16;
+        double flops = 0.0;
+        for (int p = 0; p < maxphase; ++p) {
+            int ncol = 0;
+            for (int j = 0; j < njobs; ++j)
+                if (jobs_h_[j].nphase > p) {
+                    ncol = std::max(ncol, jobs_h_[j].col + jobs_h_[j].k);
+                    flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
+                }
+            const int tiles = ((ncol + 63) / 64) * ((R + 127) / 128);
+            int splits = std::max(1, std::min({grid / std::max(tiles, 1), 16, std::max(1, kt / 2)}));
+            while (splits > 1 && (size_t)splits * R * ncol > ws_.n) --splits;
+            phase_h_[p] = std::max(ncol, 1);
+            phase_h_[kMaxPhases + p] = splits;
+        }
+        AERO_CUDA(cudaMemcpyAsync(phase_d_, phase_h_, sizeof(int) * 2 * kMaxPhases, cudaMemcpyHostToDevice, st_));
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
+        iterate_persistent(st_, jobs_d_, njobs, maxphase, R, G_.p, cap_, X_.p, ldx_, H_.p, status_d_, sig_.p,
+                           vr_.p, kv_, clamp_d_, ws_.p, phase_d_, phase_d_ + kMaxPhases, bar_d_, max_k);
+        if (profiling) {
+            AERO_CUDA(cudaEventRecord(ev_at(3), st_));
+            prof.product_launches++;
+            prof.product_flops += flops;
+        }
+        maxphase = 1;  // one timed region below
+    } else {
     if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
     iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
     for (int p = 0; p < maxphase; ++p) {
@@ -288,6 +330,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         else
             iter_normalize(st_, jobs_d_, njobs, p, X_.p, Y_.p, ldx_, H_.p, status_d_, sig_.p,
                            vr_.p, kv_, clamp_d_, std::max(max_k, 1));
+    }
     }
     if (profiling) AERO_CUDA(cudaEventRecord(ev_at(1), st_));
     AERO_CUDA(cudaMemcpyAsync(sig_h_, sig_.p, sizeof(double) * ncol_total, cudaMemcpyDeviceToHost, st_));

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <deque>
 #include <string>
 #include <vector>
@@ -128,6 +129,11 @@ class Sketch {
     // device buffers
     DeviceBuf C_, C2_, G_, E_, ew_, fw_, stage_, nrm_, X_, Y_, H_, sig_, vr_, small_, Bq_, Wq_,
         qw_, qy_, ws_;
+    static constexpr int kMaxPhases = 256;
+    int* phase_d_ = nullptr;   // per-phase active columns | split-K factors (persistent iterate)
+    int* phase_h_ = nullptr;
+    unsigned* bar_d_ = nullptr;  // grid-barrier counter of the persistent iterate
+    bool persistent_ = getenv("AERO_NO_PERSISTENT") == nullptr;  // dev A/B switch
     int* status_d_ = nullptr;
     int* clamp_d_ = nullptr;
     int* colmask_d_ = nullptr;

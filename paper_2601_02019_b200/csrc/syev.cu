@@ -43,19 +43,6 @@ constexpr int TRD_TILE = 64;      // trailing-update tile
 constexpr int SLOTW = 4;          // doubles per CTA partial slot
 constexpr int BT_NB = 128;        // reflectors per back-transform block
 
-// monotone arrival counter (zeroed before the launch): release-add, acquire-spin
-__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch, unsigned nblocks) {
-    __syncthreads();
-    epoch += nblocks;
-    if (threadIdx.x == 0) {
-        cuda::atomic_ref<unsigned, cuda::thread_scope_device> c(*ctr);
-        c.fetch_add(1u, cuda::memory_order_release);
-        while (c.load(cuda::memory_order_acquire) < epoch) {
-        }
-    }
-    __syncthreads();
-}
-
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
