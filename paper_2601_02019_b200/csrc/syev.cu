@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const dou
     __shared__ double red[64];
     extern __shared__ double dots[];  // n
     const int q = blockIdx.x;
-    const double thr = 1e-7 * bounds[3] + bounds[2];
+    const double thr = 1e-6 * bounds[3] + bounds[2];
     auto linked = [&](int i) { return i > 0 && wdesc[i - 1] - wdesc[i] <= thr; };
     // the whole run of linked eigenvalues around q
     int st = q;
