@@ -702,8 +702,8 @@ int iterate_grid(int R) {
 void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const double* G,
                         int ldg, double* X, int ldx, double* H, int* status, double* out_sig, double* out_vr,
                         int kv, int* out_clamped, double* ws, const int* phase_ncol, const int* phase_splits,
-                        unsigned* bar, int max_k) {
-    const int grid = iterate_grid(R);
+                        unsigned* bar, int max_k, int grid) {
+    grid = std::max(1, std::min(grid, iterate_grid(R)));
     AERO_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), st));
     IterPersistArgs a{jobs, njobs, maxphase, R, ldg, ldx, kv, G, X, H, out_sig, out_vr, ws, status, out_clamped,
                       phase_ncol, phase_splits, bar};

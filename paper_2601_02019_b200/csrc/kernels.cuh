@@ -74,12 +74,14 @@ void iter_normalize_ws(cudaStream_t st, const IterJob* jobs, int njobs, int phas
 // all phases of a batch in one persistent cooperative launch (max_k <= 4):
 // split-K DMMA products into ws (phase_splits[p] * R * phase_ncol[p] doubles)
 // and per-job normalization separated by grid barriers; same results as the
-// per-phase gemm_big + iter_normalize_ws sequence
-int iterate_grid(int R);  // co-resident CTAs of the persistent kernel
+// per-phase gemm_big + iter_normalize_ws sequence. `grid` (<= iterate_grid(R),
+// the co-resident maximum) is sized to the work so small problems leave the
+// rest of the GPU to concurrent streams (MlState levels)
+int iterate_grid(int R);
 void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const double* G,
                         int ldg, double* X, int ldx, double* H, int* status, double* out_sig, double* out_vr,
                         int kv, int* out_clamped, double* ws, const int* phase_ncol, const int* phase_splits,
-                        unsigned* bar, int max_k);
+                        unsigned* bar, int max_k, int grid);
 
 // ---- small dense helpers ---------------------------------------------------
 // symmetric eigendecomposition of `batch` n x n matrices (column-major, ld,

@@ -269,8 +269,16 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     const bool small_phases = big * big * (double)ncol_total < 1e8;
     if (max_k <= 4 && maxphase <= kMaxPhases && persistent_ && small_phases) {
         // all phases in one cooperative launch (kernels.cu k_iterate)
-        const int grid = iterate_grid(R);
         const int kt = (R + 15) / 16;
+        int max_tiles = 1;
+        for (int p = 0; p < maxphase; ++p) {
+            int ncol = 0;
+            for (int j = 0; j < njobs; ++j)
+                if (jobs_h_[j].nphase > p) ncol = std::max(ncol, jobs_h_[j].col + jobs_h_[j].k);
+            max_tiles = std::max(max_tiles, ((ncol + 63) / 64) * ((R + 127) / 128));
+        }
+        // CTAs: one per job for the normalizations, ~8 K-splits per product tile
+        const int grid = std::min(iterate_grid(R), std::max({njobs, 8 * max_tiles, 16}));
         double flops = 0.0;
         for (int p = 0; p < maxphase; ++p) {
             int ncol = 0;
@@ -290,7 +298,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
         iterate_persistent(st_, jobs_d_, njobs, maxphase, R, G_.p, cap_, X_.p, ldx_, H_.p, status_d_, sig_.p,
-                           vr_.p, kv_, clamp_d_, ws_.p, phase_d_, phase_d_ + kMaxPhases, bar_d_, max_k);
+                           vr_.p, kv_, clamp_d_, ws_.p, phase_d_, phase_d_ + kMaxPhases, bar_d_, max_k, grid);
         if (profiling) {
             AERO_CUDA(cudaEventRecord(ev_at(3), st_));
             prof.product_launches++;

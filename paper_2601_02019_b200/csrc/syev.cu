@@ -414,9 +414,119 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
 #undef TRD_MARK
 }
 
+// Medium n (kSytrdSmall < n <= 512): unblocked dsytd2 by ONE thread-block
+// cluster with the matrix distributed over the CTAs' shared memory (columns
+// [q cw, (q+1) cw) in CTA q, both triangles) and exchanged through DSMEM:
+// two cluster barriers per column, no global round trips on the critical path.
+template <int CS>
+__global__ void __launch_bounds__(256, 1) k_sytrd_cluster(int n, const double* __restrict__ Ain, int lda,
+                                                          double* __restrict__ V, double* __restrict__ d,
+                                                          double* __restrict__ e, double* __restrict__ tau) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    const int q = (int)cl.block_rank();
+    const int cw = (n + CS - 1) / CS;
+    const int c_lo = q * cw, c_hi = min(n, c_lo + cw);
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    double* Al = sm;                // cw x n, column c at (c - c_lo) * n
+    double* vbuf = Al + (size_t)cw * n;  // n: the owner's reflector (read remotely)
+    double* sv = vbuf + n;          // n: local copy of the reflector
+    double* w = sv + n;             // n
+    double* pbuf = w + n;           // cw: p for own columns (read remotely)
+    double* parts = pbuf + cw;      // 4: [0] partial p.v, [1] tau (owner)
+    double* red = parts + 4;        // 64
+    for (int idx = tid; idx < (c_hi - c_lo) * n; idx += nt) {
+        const int c = c_lo + idx / n, r = idx % n;
+        Al[idx] = Ain[r + (int64_t)c * lda];
+    }
+    cl.sync();
+    for (int j = 0; j < n - 1; ++j) {
+        const int owner = j / cw;
+        const int m = n - j - 1;
+        if (q == owner) {
+            const double* x = Al + (size_t)(j - c_lo) * n;
+            double s2 = 0.0;
+            for (int r = j + 2 + tid; r < n; r += nt) s2 += x[r] * x[r];
+            s2 = block_sum_d(s2, red);
+            const double alpha = x[j + 1];
+            double tj = 0.0, beta = alpha, scal = 0.0;
+            if (s2 > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+                tj = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            for (int i = tid; i < m; i += nt) {
+                const double v = (i == 0) ? 1.0 : x[j + 1 + i] * scal;
+                vbuf[i] = v;
+                V[j + 1 + i + (int64_t)j * n] = v;
+            }
+            if (tid == 0) {
+                d[j] = x[j];
+                e[j] = beta;
+                tau[j] = tj;
+                parts[1] = tj;
+            }
+        }
+        cl.sync();
+        const double* ovb = cl.map_shared_rank(vbuf, owner);
+        const double tj = *cl.map_shared_rank(parts + 1, owner);
+        if (tj == 0.0) {  // H = I: nothing to update (uniform over the cluster)
+            cl.sync();
+            continue;
+        }
+        for (int i = tid; i < m; i += nt) sv[i] = ovb[i];
+        __syncthreads();
+        // p_c = tau A(j+1:, c) . v for own columns c > j (warp per column)
+        double pv = 0.0;
+        for (int c = max(c_lo, j + 1) + warp; c < c_hi; c += nw) {
+            const double* col = Al + (size_t)(c - c_lo) * n + j + 1;
+            double acc = 0.0;
+            for (int i = lane; i < m; i += 32) acc = fma(col[i], sv[i], acc);
+            acc = warp_sum_d(acc) * tj;
+            if (lane == 0) {
+                pbuf[c - c_lo] = acc;
+                pv += acc * sv[c - j - 1];
+            }
+        }
+        pv = block_sum_d(pv, red);
+        if (tid == 0) parts[0] = pv;
+        cl.sync();
+        if (warp == 0) {  // the CS partial p.v, one remote load per lane, fixed-order tree
+            double v = (lane < CS) ? *cl.map_shared_rank(parts, lane) : 0.0;
+            v = warp_sum_d(v);
+            if (lane == 0) red[40] = v;
+        }
+        __syncthreads();
+        const double K = -0.5 * tj * red[40];
+        for (int i = tid; i < m; i += nt) {  // w = p + K v (p_r lives with the owner of column r)
+            const int r = j + 1 + i, o = r / cw;
+            w[i] = *cl.map_shared_rank(pbuf + (r - o * cw), o) + K * sv[i];
+        }
+        __syncthreads();
+        // own columns: A(j+1:, c) -= v w_c + w v_c
+        const int cfirst = max(c_lo, j + 1);
+        const int ncols = c_hi - cfirst;
+        for (int idx = tid; idx < ncols * m; idx += nt) {
+            const int c = cfirst + idx / m, i = idx % m;
+            const int ic = c - j - 1;
+            Al[(size_t)(c - c_lo) * n + j + 1 + i] -= sv[i] * w[ic] + w[i] * sv[ic];
+        }
+        __syncthreads();
+    }
+    if (q == (n - 1) / cw && tid == 0) d[n - 1] = Al[(size_t)(n - 1 - c_lo) * n + n - 1];
+    cl.sync();
+}
+
+size_t sytrd_cluster_smem(int n, int cs) {
+    const int cw = (n + cs - 1) / cs;
+    return sizeof(double) * ((size_t)cw * n + 3 * (size_t)n + cw + 4 + 64);
+}
+
 // Small n (<= kSytrdSmall): unblocked dsytd2 by ONE CTA with the whole matrix
 // in shared memory (no grid barriers). Same outputs as k_sytrd.
 constexpr int kSytrdSmall = 128;
+constexpr int kSytrdClusterMax = 512;
 __global__ void __launch_bounds__(512, 1) k_sytrd_small(int n, const double* __restrict__ Ain, int lda,
                                                         double* __restrict__ V, double* __restrict__ d,
                                                         double* __restrict__ e, double* __restrict__ tau) {
@@ -623,7 +733,7 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
                           const double* __restrict__ lam, const double* __restrict__ wdesc,
                           const int* __restrict__ order, const int* __restrict__ blk,
                           const double* __restrict__ bounds, double* __restrict__ Dp, double* __restrict__ L1,
-                          double* __restrict__ L2, double* __restrict__ L3, double* __restrict__ Z) {
+                          double* __restrict__ L2, double* __restrict__ L3, double* __restrict__ Z, int usm) {
     extern __shared__ double sde[];
     double* sd = sde;
     double* se = sde + n;
@@ -639,18 +749,23 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     const double lv = lam[p];
     const double pivmin = bounds[2];
     auto safe = [&](double x) { return (fabs(x) < pivmin) ? -pivmin : x; };
-    for (int i = 0; i < bs; ++i) Z[(int64_t)i * nvec + q] = 0.0;
-    for (int i = bt; i < n; ++i) Z[(int64_t)i * nvec + q] = 0.0;
+    // per-thread scratch in shared memory when it fits (usm), else interleaved in global
+    double* sDp = sde + 2 * n + threadIdx.x;
+    double* sZ = sDp + (size_t)n * blockDim.x;
+    auto DP = [&](int i) -> double& { return usm ? sDp[(size_t)i * blockDim.x] : Dp[(int64_t)i * nvec + q]; };
+    auto ZZ = [&](int i) -> double& { return usm ? sZ[(size_t)i * blockDim.x] : Z[(int64_t)i * nvec + q]; };
     if (bt - bs == 1) {
-        Z[(int64_t)bs * nvec + q] = 1.0;
+        for (int i = 0; i < n; ++i) Z[(int64_t)i * nvec + q] = (i == bs) ? 1.0 : 0.0;
         return;
     }
+    for (int i = 0; i < bs; ++i) ZZ(i) = 0.0;
+    for (int i = bt; i < n; ++i) ZZ(i) = 0.0;
     // top-down stationary qd: D+(i)
     double dp = safe(sd[bs] - lv);
-    Dp[(int64_t)bs * nvec + q] = dp;
+    DP(bs) = dp;
     for (int i = bs; i < bt - 1; ++i) {
         dp = safe(sd[i + 1] - lv - se[i] * (se[i] / dp));
-        Dp[(int64_t)(i + 1) * nvec + q] = dp;
+        DP(i + 1) = dp;
     }
     // numerically repeated eigenvalue (gap to a neighbour < 1e-12 ||T||): a twisted
     // vector is not determined; LAPACK dstein-style inverse iteration instead --
@@ -660,6 +775,10 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     const double tdeg = 1e-12 * bounds[3];
     const bool degen = (q > 0 && wdesc[q - 1] - wdesc[q] < tdeg) || (q + 1 < nvec && wdesc[q] - wdesc[q + 1] < tdeg);
     if (degen) {
+        if (usm) {
+            for (int i = 0; i < bs; ++i) Z[(int64_t)i * nvec + q] = 0.0;
+            for (int i = bt; i < n; ++i) Z[(int64_t)i * nvec + q] = 0.0;
+        }
         int cnt = 0;
         for (int j = q - 1; j >= 0 && wdesc[j] - wdesc[q] < 1e-10 * bounds[3]; --j) cnt += blk[order[j]] == bs;
         const double shift = lv - cnt * 10.0 * DBL_EPSILON * bounds[3];
@@ -739,14 +858,14 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     }
     // bottom-up: D-(i) into Z, twist index by min |gamma|
     double dm = safe(sd[bt - 1] - lv);
-    Z[(int64_t)(bt - 1) * nvec + q] = dm;
+    ZZ(bt - 1) = dm;
     int r = bt - 1;
     double best = fabs(dp);  // gamma at the last row = D+(last)
 #pragma unroll 4
     for (int i = bt - 2; i >= bs; --i) {
-        const double dpi = Dp[(int64_t)i * nvec + q];
+        const double dpi = DP(i);
         dm = safe(sd[i] - lv - se[i] * (se[i] / dm));
-        Z[(int64_t)i * nvec + q] = dm;
+        ZZ(i) = dm;
         const double g = dpi + dm - (sd[i] - lv);
         if (fabs(g) < best) {
             best = fabs(g);
@@ -757,22 +876,24 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     double nrm2 = 1.0, z = 1.0;
 #pragma unroll 4
     for (int i = r; i < bt - 1; ++i) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
-        const double dmn = Z[(int64_t)(i + 1) * nvec + q];
+        const double dmn = ZZ(i + 1);
         z = -(se[i] / dmn) * z;
-        Z[(int64_t)(i + 1) * nvec + q] = z;
+        ZZ(i + 1) = z;
         nrm2 += z * z;
     }
-    Z[(int64_t)r * nvec + q] = 1.0;
+    ZZ(r) = 1.0;
     z = 1.0;
 #pragma unroll 4
     for (int i = r - 1; i >= bs; --i) {  // z_i = -(e_i / D+(i)) z_{i+1}
-        z = -(se[i] / Dp[(int64_t)i * nvec + q]) * z;
-        Z[(int64_t)i * nvec + q] = z;
+        z = -(se[i] / DP(i)) * z;
+        ZZ(i) = z;
         nrm2 += z * z;
     }
     const double sc = 1.0 / sqrt(nrm2);
 #pragma unroll 4
-    for (int i = bs; i < bt; ++i) Z[(int64_t)i * nvec + q] *= sc;
+    for (int i = bs; i < bt; ++i) ZZ(i) *= sc;
+    if (usm)
+        for (int i = 0; i < n; ++i) Z[(int64_t)i * nvec + q] = ZZ(i);
 }
 
 // re-orthonormalize the vectors of each cluster of close eigenvalues
@@ -854,22 +975,28 @@ __global__ void k_interleaved_to_cols(int n, int nvec, const double* __restrict_
 // CTA per block b, T_b (nb x nb upper) from S_b = V_b^T V_b and tau, T in smem
 __global__ void k_larft(int nref, const double* __restrict__ S, const double* __restrict__ tau,
                         double* __restrict__ T) {
-    extern __shared__ double sT[];  // BT_NB x BT_NB, then one column of S
+    extern __shared__ double sT[];  // BT_NB x BT_NB T, then S strictly-upper packed by column
     const int b = blockIdx.x;
     const int j0 = b * BT_NB, nb = min(BT_NB, nref - j0);
     const double* Sb = S + (size_t)b * BT_NB * BT_NB;
-    double* scol = sT + BT_NB * BT_NB;
-    for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) sT[idx] = 0.0;
+    double* sS = sT + BT_NB * BT_NB;  // column i at offset i(i-1)/2, rows 0..i-1
+    for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) {
+        sT[idx] = 0.0;
+        const int r = idx % BT_NB, c = idx / BT_NB;
+        if (r < c) sS[c * (c - 1) / 2 + r] = Sb[r + (size_t)c * BT_NB];
+    }
     __syncthreads();
+    // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i): 4 threads per row split the sum
+    const int r = threadIdx.x >> 2, part = threadIdx.x & 3;
     for (int i = 0; i < nb; ++i) {
-        for (int r = threadIdx.x; r < i; r += blockDim.x) scol[r] = Sb[r + (size_t)i * BT_NB];
-        __syncthreads();
         const double ti = tau[j0 + i];
-        for (int r = threadIdx.x; r < i; r += blockDim.x) {  // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i)
-            double acc = 0.0;
-            for (int c = r; c < i; ++c) acc = fma(sT[r + c * BT_NB], scol[c], acc);
-            sT[r + i * BT_NB] = -ti * acc;
-        }
+        const double* scol = sS + i * (i - 1) / 2;
+        double acc = 0.0;
+        if (r < i)
+            for (int c = r + part; c < i; c += 4) acc = fma(sT[r + c * BT_NB], scol[c], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (r < i && part == 0) sT[r + i * BT_NB] = -ti * acc;
         if (threadIdx.x == 0) sT[i + i * BT_NB] = ti;
         __syncthreads();
     }
@@ -910,16 +1037,20 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
         const size_t smax = trd_smem(kEighLargeMax);
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sytrd_cluster_smem(256, 8)));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sytrd_cluster_smem(kSytrdClusterMax, 16)));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * (kSytrdSmall * kSytrdSmall + 2 * kSytrdSmall + 64))));
         AERO_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(2 * sizeof(double) * kEighLargeMax)));
-        AERO_CUDA(cudaFuncSetAttribute(k_twisted, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(2 * sizeof(double) * kEighLargeMax)));
+        AERO_CUDA(cudaFuncSetAttribute(k_twisted, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
         AERO_CUDA(cudaFuncSetAttribute(k_cluster_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * kEighLargeMax)));
         AERO_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * (BT_NB * BT_NB + BT_NB))));
+                                       (int)(sizeof(double) * (BT_NB * BT_NB + BT_NB * (BT_NB - 1) / 2))));
         int sms = 0;
         AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         wk.grid = sms;  // one CTA per SM (cooperative residency)
@@ -963,6 +1094,24 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     if (n <= kSytrdSmall) {
         k_sytrd_small<<<1, 512, sizeof(double) * ((size_t)n * n + 2 * n + 64), st>>>(n, A, lda, wk.V.p, d, e, tau);
         AERO_LAUNCHED();
+    } else if (n <= kSytrdClusterMax) {
+        const int cs = (n <= 256) ? 8 : 16;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = sytrd_cluster_smem(n, cs);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cs == 8)
+            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<8>, n, (const double*)A, lda, wk.V.p, d, e, tau));
+        else
+            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<16>, n, (const double*)A, lda, wk.V.p, d, e, tau));
     } else {
         AERO_CUDA(cudaLaunchCooperativeKernel(vec ? (void*)k_sytrd<true> : (void*)k_sytrd<false>, dim3(G),
                                               dim3(TRD_THREADS), args, smem, st));
@@ -993,8 +1142,15 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     wk.Z.alloc((size_t)n * nvec);
     note_launch();
     wk.L.alloc((size_t)3 * n * nvec);
-    k_twisted<<<(nvec + 31) / 32, 32, sde, st>>>(n, nvec, d, e, lam, w, order, blk, bounds, wk.Dp.p, wk.L.p,
-                                                 wk.L.p + (size_t)n * nvec, wk.L.p + (size_t)2 * n * nvec, wk.Z.p);
+    {  // per-thread scratch in shared memory when 2 n x threads doubles fit
+        int tb = 32;
+        while (tb > 4 && sde + 2 * sizeof(double) * (size_t)n * tb > 200 * 1024) tb /= 2;
+        const bool usm = sde + 2 * sizeof(double) * (size_t)n * tb <= 200 * 1024;
+        const size_t sm_tw = sde + (usm ? 2 * sizeof(double) * (size_t)n * tb : 0);
+        k_twisted<<<(nvec + tb - 1) / tb, tb, sm_tw, st>>>(n, nvec, d, e, lam, w, order, blk, bounds, wk.Dp.p,
+                                                          wk.L.p, wk.L.p + (size_t)n * nvec,
+                                                          wk.L.p + (size_t)2 * n * nvec, wk.Z.p, usm ? 1 : 0);
+    }
     AERO_LAUNCHED();
     note_launch();
     k_cluster_orth<<<nvec, 256, sizeof(double) * (size_t)n, st>>>(n, nvec, w, bounds, wk.Z.p);
@@ -1022,7 +1178,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
                  wk.ws.p, wsn);
     }
     note_launch();
-    k_larft<<<nblk, 128, sizeof(double) * (BT_NB * BT_NB + BT_NB), st>>>(nref, wk.S.p, tau, wk.T.p);
+    k_larft<<<nblk, 4 * BT_NB, sizeof(double) * (BT_NB * BT_NB + BT_NB * (BT_NB - 1) / 2), st>>>(nref, wk.S.p, tau, wk.T.p);
     AERO_LAUNCHED();
     for (int b = nblk - 1; b >= 0; --b) {
         const int j0 = b * BT_NB, nb = std::min(BT_NB, nref - j0), mr = n - j0;
