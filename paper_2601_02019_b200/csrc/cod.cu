@@ -467,7 +467,7 @@ struct CodEngine::Impl {
         scale_columns(st, ra, rb, K, ra, q2.p + m);
         // SVD of K via eig(K K^T): u (ra x ra, descending), s^2
         dgemm(st, false, true, ra, ra, rb, 1.0, K, ra, K, ra, 0.0, T, ra);
-        eigh(st, ra, T, ra, ls);
+        eigh(st, ra, T, ra, ls, 1, 0, std::min(ra, keep + 1));  // the kept directions (and the cut)
         std::vector<double> hl(ra);
         AERO_CUDA(cudaMemcpyAsync(hl.data(), ls, sizeof(double) * ra, cudaMemcpyDeviceToHost, st));
         AERO_CUDA(cudaStreamSynchronize(st));

@@ -165,11 +165,6 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
                 const int i = c - (j + 1);
                 sv[c - c0] = (c >= n || i < 0) ? 0.0 : (i == 0 ? 1.0 : sx[i + 1] * scal);
             }
-            if (nxt && tid < jj) {  // row j+1 of the panel (W(j+1, jj-1) not yet in W)
-                srow[tid] = (tid == jj - 1) ? __ldcg(a.wpre + j + 1) + a2prev * svo[j + 1 - c0prev]
-                                            : __ldcg(W + j + 1 + (int64_t)tid * n);
-                srow[TRD_NB + tid] = __ldcg(V + j + 1 + (int64_t)(i0 + tid) * n);
-            }
             if (cta == 0 && tid == 0) {
                 a.d[j] = sx[0];
                 a.e[j] = beta;
@@ -309,6 +304,11 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
             // ---- A': finish W(:, jj) (own rows), next column into sx
             double yv[16];
             const double wj1 = nxt ? __ldcg(a.wpre + j + 1) : 0.0;
+            // row j+2 of the panel for the next column's y0 (srow), loaded with the rest
+            const bool pre = nxt && tid <= jj && j + 2 < n;
+            const double wj2 = (pre && tid == jj) ? __ldcg(a.wpre + j + 2) : 0.0;
+            const double sr_w = (pre && tid < jj) ? __ldcg(W + j + 2 + (int64_t)tid * n) : 0.0;
+            const double sr_v = pre ? __ldcg(V + j + 2 + (int64_t)(i0 + tid) * n) : 0.0;
             if (nxt) {
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
@@ -329,6 +329,10 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
                         sx[rr - j - 1] = x;
                         if (rr >= j + 3) s2p += x * x;
                     }
+                }
+                if (pre) {
+                    srow[tid] = (tid == jj) ? wj2 + a2 * sv[j + 2 - c0] : sr_w;
+                    srow[TRD_NB + tid] = sr_v;
                 }
                 a2prev = a2;
                 c0prev = c0;
@@ -665,6 +669,37 @@ __device__ __forceinline__ int sturm_count(int s, int t, const double* d, const 
     return cnt;
 }
 
+// lower end of the bisection interval of the kc-th smallest eigenvalue of the
+// whole (split) T -> bounds[4]; eigenvalues certainly below it are not needed
+// when only the top n - kc are (one warp, 33-way multisection)
+__global__ void k_cut(int n, int kc, const double* __restrict__ d, const double* __restrict__ e2,
+                      double* __restrict__ bounds) {
+    const int lane = threadIdx.x & 31;
+    const double pivmin = bounds[2];
+    double lo = bounds[0], hi = bounds[1];
+    for (int round = 0; round < 64; ++round) {
+        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
+        if (hi - lo <= tol) break;
+        const double h = (hi - lo) / 33.0;
+        const double x = fmin(lo + h * (lane + 1), hi);
+        const int c = sturm_count(0, n, d, e2, x, pivmin);
+        const unsigned above = __ballot_sync(0xffffffffu, c > kc);
+        double nlo = lo, nhi = hi;
+        if (above) {
+            const int f = __ffs(above) - 1;
+            nhi = __shfl_sync(0xffffffffu, x, f);
+            const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+            if (f > 0) nlo = xp;
+        } else {
+            nlo = __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (nlo == lo && nhi == hi) break;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) bounds[4] = lo - 2.0 * DBL_EPSILON * fabs(lo) - pivmin;
+}
+
 // one warp per row p: the (p - s)-th smallest eigenvalue of p's block [s, t),
 // by 33-way multisection of the Gershgorin interval; d, e^2 in shared memory
 __global__ void k_bisect(int n, const double* __restrict__ d, const double* __restrict__ e2,
@@ -688,6 +723,11 @@ __global__ void k_bisect(int n, const double* __restrict__ d, const double* __re
     }
     const double pivmin = bounds[2];
     double lo = bounds[0], hi = bounds[1];
+    // below the cut (only the top eigenvalues are wanted): park at the lower bound
+    if (sturm_count(bs, bt, sd, se, bounds[4], pivmin) > k) {
+        if (lane == 0) lam[p] = lo;
+        return;
+    }
     for (int round = 0; round < 64; ++round) {
         const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
         if (hi - lo <= tol) break;
@@ -1131,6 +1171,14 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     AERO_LAUNCHED();
     const size_t sde = 2 * sizeof(double) * (size_t)n;
     note_launch();
+    if (nvec < n - 1) {  // only the top nvec + 1 eigenvalues are needed
+        note_launch();
+        k_cut<<<1, 32, 0, st>>>(n, n - nvec - 1, d, e2, bounds);
+        AERO_LAUNCHED();
+    } else {
+        const double ninf = -DBL_MAX;
+        AERO_CUDA(cudaMemcpyAsync(bounds + 4, &ninf, sizeof(double), cudaMemcpyHostToDevice, st));
+    }
     k_bisect<<<(n * 32 + 127) / 128, 128, sde, st>>>(n, d, e2, bounds, blk, lam);
     AERO_LAUNCHED();
     note_launch();
@@ -1168,7 +1216,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     wk.T.alloc((size_t)nblk * BT_NB * BT_NB);
     wk.M1.alloc((size_t)BT_NB * nvec);
     wk.M2.alloc((size_t)BT_NB * nvec);
-    const size_t wsn = (size_t)8 * BT_NB * std::max(nvec, BT_NB);  // split-K partials of skinny products
+    const size_t wsn = std::max((size_t)8 * BT_NB * std::max(nvec, BT_NB), (size_t)4 * n * nvec);  // split-K partials
     wk.ws.alloc(wsn);
     // row j0 of block b is zero in every reflector of the block: start there (keeps 16 B alignment)
     for (int b = 0; b < nblk; ++b) {
