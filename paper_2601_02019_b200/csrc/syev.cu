@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
 template <int CS>
 __global__ void __launch_bounds__(256, 1) k_sytrd_cluster(int n, const double* __restrict__ Ain, int lda,
                                                           double* __restrict__ V, double* __restrict__ d,
-                                                          double* __restrict__ e, double* __restrict__ tau) {
+                                                          double* __restrict__ e, double* __restrict__ tau,
+                                                          unsigned long long* prof) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
@@ -433,81 +434,88 @@ __global__ void __launch_bounds__(256, 1) k_sytrd_cluster(int n, const double* _
     const int cw = (n + CS - 1) / CS;
     const int c_lo = q * cw, c_hi = min(n, c_lo + cw);
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    double* Al = sm;                // cw x n, column c at (c - c_lo) * n
-    double* vbuf = Al + (size_t)cw * n;  // n: the owner's reflector (read remotely)
-    double* sv = vbuf + n;          // n: local copy of the reflector
-    double* w = sv + n;             // n
-    double* pbuf = w + n;           // cw: p for own columns (read remotely)
-    double* parts = pbuf + cw;      // 4: [0] partial p.v, [1] tau (owner)
-    double* red = parts + 4;        // 64
+    // reflector, p values and partials are double-buffered by column parity, so
+    // the owner of column j+1 can push before slower CTAs finish column j
+    double* Al = sm;                     // cw x n, column c at (c - c_lo) * n
+    double* svb = Al + (size_t)cw * n;   // 2 n: reflector, PUSHED here by its owner
+    double* pwb = svb + 2 * n;           // 2 n: p values of all columns, pushed by their owners
+    double* w = pwb + 2 * n;             // n
+    double* partsb = w + n;              // 2 (CS + 4): partial p.v (pushed) | [CS] tau (pushed)
+    double* red = partsb + 2 * (CS + 4); // 64
     for (int idx = tid; idx < (c_hi - c_lo) * n; idx += nt) {
         const int c = c_lo + idx / n, r = idx % n;
         Al[idx] = Ain[r + (int64_t)c * lda];
     }
     cl.sync();
+    unsigned long long tp = clock64();
+#define CL_MARK(i)                                          \
+    if (prof && q == 0 && tid == 0) {                       \
+        const unsigned long long t_ = clock64();            \
+        prof[i] += t_ - tp;                                 \
+        tp = t_;                                            \
+    }
     for (int j = 0; j < n - 1; ++j) {
         const int owner = j / cw;
         const int m = n - j - 1;
-        if (q == owner) {
+        double* sv = svb + (j & 1) * n;
+        double* pw = pwb + (j & 1) * n;
+        double* parts = partsb + (j & 1) * (CS + 4);
+        if (q == owner) {  // reflector of column j (warp 0 reduces), pushed to every CTA
             const double* x = Al + (size_t)(j - c_lo) * n;
-            double s2 = 0.0;
-            for (int r = j + 2 + tid; r < n; r += nt) s2 += x[r] * x[r];
-            s2 = block_sum_d(s2, red);
-            const double alpha = x[j + 1];
-            double tj = 0.0, beta = alpha, scal = 0.0;
-            if (s2 > 0.0) {
-                beta = -copysign(sqrt(alpha * alpha + s2), alpha);
-                tj = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
+            if (warp == 0) {
+                double s2 = 0.0;
+                for (int r = j + 2 + lane; r < n; r += 32) s2 += x[r] * x[r];
+                s2 = warp_sum_d(s2);
+                if (lane == 0) {
+                    const double alpha = x[j + 1];
+                    double tj = 0.0, beta = alpha, scal = 0.0;
+                    if (s2 > 0.0) {
+                        beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+                        tj = (beta - alpha) / beta;
+                        scal = 1.0 / (alpha - beta);
+                    }
+                    red[40] = tj;
+                    red[41] = scal;
+                    d[j] = x[j];
+                    e[j] = beta;
+                    tau[j] = tj;
+                }
             }
+            __syncthreads();
+            const double tj = red[40], scal = red[41];
             for (int i = tid; i < m; i += nt) {
                 const double v = (i == 0) ? 1.0 : x[j + 1 + i] * scal;
-                vbuf[i] = v;
                 V[j + 1 + i + (int64_t)j * n] = v;
+                for (int r = 0; r < CS; ++r) cl.map_shared_rank(sv, r)[i] = v;
             }
-            if (tid == 0) {
-                d[j] = x[j];
-                e[j] = beta;
-                tau[j] = tj;
-                parts[1] = tj;
-            }
+            if (tid < CS) cl.map_shared_rank(parts, tid)[CS] = tj;
         }
+        CL_MARK(0);
         cl.sync();
-        const double* ovb = cl.map_shared_rank(vbuf, owner);
-        const double tj = *cl.map_shared_rank(parts + 1, owner);
-        if (tj == 0.0) {  // H = I: nothing to update (uniform over the cluster)
-            cl.sync();
-            continue;
-        }
-        for (int i = tid; i < m; i += nt) sv[i] = ovb[i];
-        __syncthreads();
-        // p_c = tau A(j+1:, c) . v for own columns c > j (warp per column)
+        CL_MARK(1);
+        const double tj = parts[CS];
+        if (tj == 0.0) continue;  // H = I: nothing to update (uniform over the cluster)
+        // p_c = tau A(j+1:, c) . v for own columns c > j (warp per column), pushed to all CTAs
         double pv = 0.0;
         for (int c = max(c_lo, j + 1) + warp; c < c_hi; c += nw) {
             const double* col = Al + (size_t)(c - c_lo) * n + j + 1;
             double acc = 0.0;
             for (int i = lane; i < m; i += 32) acc = fma(col[i], sv[i], acc);
             acc = warp_sum_d(acc) * tj;
-            if (lane == 0) {
-                pbuf[c - c_lo] = acc;
-                pv += acc * sv[c - j - 1];
-            }
+            if (lane < CS) cl.map_shared_rank(pw, lane)[c] = acc;
+            if (lane == 0) pv += acc * sv[c - j - 1];
         }
         pv = block_sum_d(pv, red);
-        if (tid == 0) parts[0] = pv;
+        if (tid < CS) cl.map_shared_rank(parts, tid)[q] = pv;
+        CL_MARK(3);
         cl.sync();
-        if (warp == 0) {  // the CS partial p.v, one remote load per lane, fixed-order tree
-            double v = (lane < CS) ? *cl.map_shared_rank(parts, lane) : 0.0;
-            v = warp_sum_d(v);
-            if (lane == 0) red[40] = v;
-        }
+        CL_MARK(4);
+        double tot = 0.0;
+        for (int r = 0; r < CS; ++r) tot += parts[r];  // fixed order
+        const double K = -0.5 * tj * tot;
+        for (int i = tid; i < m; i += nt) w[i] = pw[j + 1 + i] + K * sv[i];
         __syncthreads();
-        const double K = -0.5 * tj * red[40];
-        for (int i = tid; i < m; i += nt) {  // w = p + K v (p_r lives with the owner of column r)
-            const int r = j + 1 + i, o = r / cw;
-            w[i] = *cl.map_shared_rank(pbuf + (r - o * cw), o) + K * sv[i];
-        }
-        __syncthreads();
+        CL_MARK(5);
         // own columns: A(j+1:, c) -= v w_c + w v_c
         const int cfirst = max(c_lo, j + 1);
         const int ncols = c_hi - cfirst;
@@ -516,15 +524,17 @@ __global__ void __launch_bounds__(256, 1) k_sytrd_cluster(int n, const double* _
             const int ic = c - j - 1;
             Al[(size_t)(c - c_lo) * n + j + 1 + i] -= sv[i] * w[ic] + w[i] * sv[ic];
         }
-        __syncthreads();
+        __syncthreads();  // the owner of column j+1 reads its (updated) column next
+        CL_MARK(6);
     }
+#undef CL_MARK
     if (q == (n - 1) / cw && tid == 0) d[n - 1] = Al[(size_t)(n - 1 - c_lo) * n + n - 1];
     cl.sync();
 }
 
 size_t sytrd_cluster_smem(int n, int cs) {
     const int cw = (n + cs - 1) / cs;
-    return sizeof(double) * ((size_t)cw * n + 3 * (size_t)n + cw + 4 + 64);
+    return sizeof(double) * ((size_t)cw * n + 5 * (size_t)n + 2 * (cs + 4) + 64);
 }
 
 // Small n (<= kSytrdSmall): unblocked dsytd2 by ONE CTA with the whole matrix
@@ -1148,10 +1158,24 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
+        static const bool cl_prof = getenv("AERO_SYTRD_PROF") != nullptr;
+        unsigned long long* cprof = nullptr;
+        if (cl_prof) {
+            AERO_CUDA(cudaMalloc(&cprof, 8 * sizeof(unsigned long long)));
+            AERO_CUDA(cudaMemsetAsync(cprof, 0, 8 * sizeof(unsigned long long), st));
+        }
         if (cs == 8)
-            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<8>, n, (const double*)A, lda, wk.V.p, d, e, tau));
+            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<8>, n, (const double*)A, lda, wk.V.p, d, e, tau, cprof));
         else
-            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<16>, n, (const double*)A, lda, wk.V.p, d, e, tau));
+            AERO_CUDA(cudaLaunchKernelEx(&cfg, k_sytrd_cluster<16>, n, (const double*)A, lda, wk.V.p, d, e, tau, cprof));
+        if (cprof) {
+            unsigned long long h[8];
+            AERO_CUDA(cudaMemcpyAsync(h, cprof, sizeof(h), cudaMemcpyDeviceToHost, st));
+            AERO_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "sytrd_cluster n=%d cs=%d kcycles: own %.0f sync1 %.0f - %.0f symv %.0f sync2 %.0f w %.0f upd %.0f\n",
+                    n, cs, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3);
+            cudaFree(cprof);
+        }
     } else {
         AERO_CUDA(cudaLaunchCooperativeKernel(vec ? (void*)k_sytrd<true> : (void*)k_sytrd<false>, dim3(G),
                                               dim3(TRD_THREADS), args, smem, st));
