@@ -137,6 +137,26 @@ def cpu_oracle_rate(cfg, nrows, threads):
     return nrows / dt, dt
 
 
+def reference_literal_flops(ev, d, ell):
+    """SURVEY.md section 8(d) F_row: the reference's own flop count per row
+    (power-iteration gate, simul_iter doubling calls, FD reduce by SVD, dumps),
+    evaluated on this run's event log."""
+    import math
+    import numpy as np
+    kp = math.ceil(math.log2(d)) + 1
+    q = math.ceil(math.log2(d) / 0.4)
+    r = ev["rows_after"].astype(np.float64)
+    f = (4 * kp + 2) * d * r * (ev["gate_fired"] >= 0)
+    steps = ev["doubling_steps"].astype(np.int64)
+    for s_ in range(1, int(steps.max()) + 1 if len(steps) else 1):
+        k = np.minimum(2.0 ** s_, r)
+        on = steps >= s_
+        f = f + on * ((4 * q + 4) * d * r * k + (8 * q + 10) * d * k * k)
+    red = 2 * (2 * ell) ** 2 * d + 9 * (2 * ell) ** 3 + 2 * (ell - 1) * (2 * ell) * d
+    f = f + ev["reduced"].astype(np.float64) * float(red) + 8.0 * r * d * ev["xi"].astype(np.float64)
+    return float(f.mean())
+
+
 def run_reference(args, cfg, rank):
     """--impl reference: the reference path's CPU implementation (the oracle
     port; the reference C++ needs Eigen, absent here) on all host threads."""
@@ -441,6 +461,12 @@ def main():
                     "product_share_of_step": prof["product_ms"] / ms_p,
                     "flops_per_launch": prof["product_flops"] / max(1, prof["product_launches"]),
                     "ms_per_launch": prof["product_ms"] / max(1, prof["product_launches"])}
+        f_row = reference_literal_flops(ev, d, info.ell)
+        path = {"f_row_gflop": f_row / 1e9, "peak_tflops": peak, "bound_rows_per_s": peak * 1e12 / f_row,
+                "frac": value / (peak * 1e12 / f_row),
+                "basis": "SURVEY.md 8(d): reference-literal flops per row (gate (4kp+2)dr, simul_iter "
+                         "(4q+4)drk+(8q+10)dk^2 per doubling call, SVD reduce, 8rd*xi dumps) from this run's "
+                         "event log, at the measured fp64 DGEMM peak; the Gram-form engine executes fewer"}
         cpu = None
         if not args.no_cpu:
             threads = 1
@@ -457,7 +483,8 @@ def main():
                        "ell": info.ell, "timed_rows": f"{warm * S + 1}..{nrows}",
                        "l2": f"inputs larger than L2 ({S * d * 8 / 2**20:.0f} MiB per step)",
                        "parallelism": "replicas" if world > 1 else "single"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roofline, "path_roofline": path, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches),
             "clocks": clocks,
             "stats": {"gate_fire_rate": float(ev["gate_fired"].mean()), "dump_rate": float(ev["dumped"].mean()),
                       "reduces": int(ev["reduced"].sum()), "batches": int(info.device_batches),
