@@ -224,6 +224,40 @@ def test_large_ell_path_parity(orc):
     assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-8
 
 
+def test_grid_eigensolver_reduce_path_parity(orc):
+    """ell=512 (2ell=1024 > 512): the reduce runs the persistent-grid
+    tridiagonalization; two reduces inside the stream."""
+    d, n = 1024, 2200
+    orc.set_threads(8)
+    rows = orc.gen_rows(d, 64, 0.97, 0.05, 64.0, 6, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, 1 / 256, 6, 1000)
+    ev_ref = ref.update_block(rows, ts)
+    orc.set_threads(1)
+    s = prod.AttpState(d, 1 / 256, seed=6, stream=1000)
+    ev = s.update_block(rows, ts)
+    assert ev_ref["reduced"].sum() >= 2
+    assert_trace_equal(ev, ev_ref, rtol=1e-7)
+    assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-8
+
+
+def test_persistent_iterate_matches_launch_sequence(orc, monkeypatch):
+    """The persistent cooperative iteration kernel and the per-phase launch
+    sequence (product + normalize) give the same decisions and sketch."""
+    n = 900
+    rows = c1_rows(orc, n)
+    ts = np.arange(1, n + 1)
+    a = prod.AttpState(1024, 1 / 16, seed=1, stream=1000)
+    ev_a = a.update_block(rows, ts)
+    monkeypatch.setenv("AERO_NO_PERSISTENT", "1")
+    b = prod.AttpState(1024, 1 / 16, seed=1, stream=1000)
+    ev_b = b.update_block(rows, ts)
+    assert_trace_equal(ev_a, ev_b, rtol=1e-9)
+    assert rel_fro(a.query_gram(0, n), b.query_gram(0, n)) < 1e-11
+    ref = orc.AttpState(1024, 1 / 16, 1, 1000)
+    assert_trace_equal(ev_a, ref.update_block(rows, ts))
+
+
 # ---------------------------------------------------------------- sliding window
 @pytest.mark.parametrize("n_win,scale_rows", [(500, ()), (50, (100, 700, 1200))])
 def test_ml_bookkeeping_bit_exact(orc, n_win, scale_rows):
