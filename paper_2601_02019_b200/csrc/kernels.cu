@@ -713,6 +713,232 @@ void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int max
                                           dim3(tiles::PNT), args, iterate_smem_bytes(R), st));
 }
 
+// ---- small buffers (r <= 96, k <= 2): one WARP per job, all phases ----------
+// Jobs of a batch only share G (read-only), so with G in shared memory every
+// job runs its whole power / subspace iteration independently: lanes own rows
+// (i = lane + 32 t), matvecs from shared memory, reductions by shuffles; no
+// grid-wide phase synchronisation at all. Same arithmetic as normalize_job.
+constexpr int kWarpIterMaxR = 96;
+constexpr int kWarpIterWarps = 8;
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void eig2_closed(double a, double b, double c, double& l0, double& l1, double T[4]) {
+    // GVL Alg. 8.4.1 rotation (same formulas as small_eig)
+    double cn = 1.0, sn = 0.0, t = 0.0;
+    if (fabs(b) > 1e-300) {
+        const double tau = (c - a) / (2.0 * b);
+        t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        cn = 1.0 / sqrt(1.0 + t * t);
+        sn = t * cn;
+    }
+    l0 = a - t * b;
+    l1 = c + t * b;
+    T[0] = cn;
+    T[1] = -sn;
+    T[2] = sn;
+    T[3] = cn;
+}
+
+__global__ void __launch_bounds__(32 * kWarpIterWarps) k_iterate_warp(
+    const IterJob* __restrict__ jobs, int njobs, const double* __restrict__ G, int ldg, int R,
+    double* __restrict__ X, int ldx, double* __restrict__ H, int* __restrict__ status,
+    double* __restrict__ out_sig, double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped) {
+    extern __shared__ double smw[];
+    double* sG = smw;  // R x R, ld R
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xs = smw + (size_t)R * R + (size_t)warp * 2 * R;  // this warp's x (2 columns, ld R)
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) sG[e] = G[e % R + (int64_t)(e / R) * ldg];
+    __syncthreads();
+    const int j = blockIdx.x * kWarpIterWarps + warp;
+    if (j >= njobs) return;
+    const IterJob jb = jobs[j];
+    const int r = jb.r, k = jb.k;
+    double* xg = X + (int64_t)jb.col * ldx;
+    if (status[j] != JOB_ACTIVE) {
+        if (lane < k) out_sig[jb.col + lane] = 0.0;
+        return;
+    }
+    constexpr int RT = kWarpIterMaxR / 32;
+    double x[RT][2], y[RT][2];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+        const int i = lane + 32 * t;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            x[t][a] = (i < r && a < k) ? xg[i + (int64_t)a * ldx] : 0.0;
+            if (i < R) xs[i + a * R] = x[t][a];
+        }
+    }
+    __syncwarp();
+    for (int p = 0; p < jb.nphase; ++p) {
+        const bool last = (p == jb.nphase - 1);
+        // y = G x (rows < r)
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int i = lane + 32 * t;
+            double y0 = 0.0, y1 = 0.0;
+            if (i < r) {
+                for (int l = 0; l < r; ++l) {
+                    const double g = sG[i + l * R];
+                    y0 = fma(g, xs[l], y0);
+                    y1 = fma(g, xs[l + R], y1);
+                }
+            }
+            y[t][0] = y0;
+            y[t][1] = (k > 1) ? y1 : 0.0;
+        }
+        if (jb.type == 0) {
+            if (!last) {
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t < RT; ++t) s = fma(y[t][0], y[t][0], s);
+                s = wsum(s);
+                const double nrm = sqrt(s);
+                if (nrm < 1e-300) {  // linalg.cpp:112-116
+                    if (lane == 0) status[j] = JOB_DEAD;
+                    return;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int i = lane + 32 * t;
+                    x[t][0] = (i < r) ? y[t][0] / nrm : 0.0;
+                    if (i < R) xs[i] = x[t][0];
+                }
+                __syncwarp();
+            } else {
+                double s = 0.0;  // sigma1^2 = x^T G x (linalg.cpp:119)
+#pragma unroll
+                for (int t = 0; t < RT; ++t) s = fma(x[t][0], y[t][0], s);
+                s = wsum(s);
+                if (lane == 0) out_sig[jb.col] = s;
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int i = lane + 32 * t;
+                    if (i < r) xg[i] = x[t][0];
+                }
+            }
+            continue;
+        }
+        // simul: S = X^T Y, T = S^{-1/2} (closed-form 2x2 / scalar), clamp
+        double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            s00 = fma(x[t][0], y[t][0], s00);
+            s01 = fma(x[t][0], y[t][1], s01);
+            s10 = fma(x[t][1], y[t][0], s10);
+            s11 = fma(x[t][1], y[t][1], s11);
+        }
+        s00 = wsum(s00);
+        s01 = wsum(s01);
+        s10 = wsum(s10);
+        s11 = wsum(s11);
+        double Tm[4], l0, l1;
+        if (k == 1) {
+            l0 = s00;
+            l1 = 0.0;
+            Tm[0] = 1.0;
+            Tm[1] = Tm[2] = 0.0;
+            Tm[3] = 1.0;
+        } else {
+            eig2_closed(s00, 0.5 * (s01 + s10), s11, l0, l1, Tm);
+        }
+        const double lmax = (k == 1) ? fmax(l0, 0.0) : fmax(fmax(l0, l1), 0.0);
+        const bool ok0 = l0 > 0.0 && l0 > 1e-14 * lmax, ok1 = (k > 1) && l1 > 0.0 && l1 > 1e-14 * lmax;
+        const double i0 = ok0 ? 1.0 / sqrt(l0) : 0.0, i1 = ok1 ? 1.0 / sqrt(l1) : 0.0;
+        if (last && out_clamped && lane == 0) out_clamped[j] = (!ok0) + (k > 1 && !ok1);
+        Tm[0] *= i0;
+        Tm[1] *= i0;
+        Tm[2] *= i1;
+        Tm[3] *= i1;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int i = lane + 32 * t;
+            const double h0 = fma(x[t][0], Tm[0], (k > 1) ? x[t][1] * Tm[1] : 0.0);
+            const double h1 = fma(x[t][0], Tm[2], (k > 1) ? x[t][1] * Tm[3] : 0.0);
+            const double n0 = fma(y[t][0], Tm[0], (k > 1) ? y[t][1] * Tm[1] : 0.0);
+            const double n1 = fma(y[t][0], Tm[2], (k > 1) ? y[t][1] * Tm[3] : 0.0);
+            if (last && i < r) {
+                H[i + (int64_t)jb.col * ldx] = h0;
+                if (k > 1) H[i + (int64_t)(jb.col + 1) * ldx] = h1;
+            }
+            x[t][0] = (i < r) ? n0 : 0.0;
+            x[t][1] = (i < r && k > 1) ? n1 : 0.0;
+            if (i < R) {
+                xs[i] = x[t][0];
+                xs[i + R] = x[t][1];
+            }
+        }
+        __syncwarp();
+        if (!last) continue;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int i = lane + 32 * t;
+            if (i < r) {
+                xg[i] = x[t][0];
+                if (k > 1) xg[i + ldx] = x[t][1];
+            }
+        }
+        // Ritz values: eig(X^T X) (linalg.cpp:145-150), sorted descending, sign-fixed
+        double w00 = 0.0, w01 = 0.0, w11 = 0.0;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            w00 = fma(x[t][0], x[t][0], w00);
+            w01 = fma(x[t][0], x[t][1], w01);
+            w11 = fma(x[t][1], x[t][1], w11);
+        }
+        w00 = wsum(w00);
+        w01 = wsum(w01);
+        w11 = wsum(w11);
+        if (lane == 0) {
+            double* vr = out_vr + (int64_t)jb.col * kv;
+            if (k == 1) {
+                out_sig[jb.col] = sqrt(fmax(w00, 0.0));
+                vr[0] = 1.0;
+            } else {
+                double V2[4], a0, a1;
+                eig2_closed(w00, w01, w11, a0, a1, V2);
+                // rank (descending, ties by index) and sign fix as cta_sort_signfix
+                const int r0 = (a1 > a0) ? 1 : 0, r1 = (a0 >= a1) ? 1 : 0;
+                const double lam[2] = {a0, a1};
+                for (int c = 0; c < 2; ++c) {
+                    const int rk = (c == 0) ? r0 : r1;
+                    const double v0 = V2[2 * c], v1 = V2[2 * c + 1];
+                    const int at = (fabs(v1) > fabs(v0)) ? 1 : 0;
+                    const double sg = ((at ? v1 : v0) < 0.0) ? -1.0 : 1.0;
+                    vr[0 + rk * 2] = sg * v0;
+                    vr[1 + rk * 2] = sg * v1;
+                    out_sig[jb.col + rk] = sqrt(fmax(lam[c], 0.0));
+                }
+            }
+        }
+    }
+}
+
+bool iterate_warp(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
+                  int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
+                  int max_k) {
+    if (R > kWarpIterMaxR || max_k > 2 || njobs <= 0) return false;
+    const size_t smem = sizeof(double) * ((size_t)R * R + (size_t)kWarpIterWarps * 2 * R);
+    static bool attr = false;
+    if (!attr) {
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * (kWarpIterMaxR * kWarpIterMaxR +
+                                                               kWarpIterWarps * 2 * kWarpIterMaxR))));
+        attr = true;
+    }
+    k_iterate_warp<<<(njobs + kWarpIterWarps - 1) / kWarpIterWarps, 32 * kWarpIterWarps, smem, st>>>(
+        jobs, njobs, G, ldg, R, X, ldx, H, status, out_sig, out_vr, kv, out_clamped);
+    AERO_LAUNCHED();
+    return true;
+}
+
 void iter_normalize(cudaStream_t st, const IterJob* jobs, int njobs, int phase, double* X,
                     const double* Y, int ldx, double* H, int* status, double* out_sig,
                     double* out_vr, int kv, int* out_clamped, int max_k) {

@@ -83,6 +83,12 @@ void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int max
                         int kv, int* out_clamped, double* ws, const int* phase_ncol, const int* phase_splits,
                         unsigned* bar, int max_k, int grid);
 
+// buffers of <= 96 rows and k <= 2: one warp per job runs all its phases with
+// G in shared memory (no phase synchronisation); returns false if not applicable
+bool iterate_warp(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
+                  int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
+                  int max_k);
+
 // ---- small dense helpers ---------------------------------------------------
 // symmetric eigendecomposition of `batch` n x n matrices (column-major, ld,
 // stride between matrices): eigenvalues descending, eigenvector columns

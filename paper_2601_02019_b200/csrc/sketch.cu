@@ -267,7 +267,22 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     double big = 0.0;
     for (int j = 0; j < njobs; ++j) big = std::max(big, (double)jobs_h_[j].r);
     const bool small_phases = big * big * (double)ncol_total < 1e8;
-    if (max_k <= 4 && maxphase <= kMaxPhases && persistent_ && small_phases) {
+    if (persistent_ && R <= 96 && max_k <= 2) {
+        // small buffer: one warp per job, all phases, G in shared memory
+        double flops = 0.0;
+        for (int j = 0; j < njobs; ++j) flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k * jobs_h_[j].nphase;
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
+        iterate_warp(st_, jobs_d_, njobs, G_.p, cap_, R, X_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p, kv_, clamp_d_,
+                     max_k);
+        if (profiling) {
+            AERO_CUDA(cudaEventRecord(ev_at(3), st_));
+            prof.product_launches++;
+            prof.product_flops += flops;
+        }
+        maxphase = 1;
+    } else if (max_k <= 4 && maxphase <= kMaxPhases && persistent_ && small_phases) {
         // all phases in one cooperative launch (kernels.cu k_iterate)
         const int kt = (R + 15) / 16;
         int max_tiles = 1;
