@@ -1142,7 +1142,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     const bool vec = !(lda & 1) && !((uintptr_t)A & 15);
     note_launch();
     if (n <= kSytrdSmall) {
-        k_sytrd_small<<<1, 512, sizeof(double) * ((size_t)n * n + 2 * n + 64), st>>>(n, A, lda, wk.V.p, d, e, tau);
+        k_sytrd_small<<<1, n <= 64 ? 128 : 512, sizeof(double) * ((size_t)n * n + 2 * n + 64), st>>>(n, A, lda, wk.V.p,
+                                                                                                      d, e, tau);
         AERO_LAUNCHED();
     } else if (n <= kSytrdClusterMax) {
         const int cs = (n <= 256) ? 8 : 16;
@@ -1195,7 +1196,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     AERO_LAUNCHED();
     const size_t sde = 2 * sizeof(double) * (size_t)n;
     note_launch();
-    if (nvec < n - 1) {  // only the top nvec + 1 eigenvalues are needed
+    if (nvec < n - 1 && n >= 512) {  // only the top nvec + 1 eigenvalues are needed
         note_launch();
         k_cut<<<1, 32, 0, st>>>(n, n - nvec - 1, d, e2, bounds);
         AERO_LAUNCHED();
