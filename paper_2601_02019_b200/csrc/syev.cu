@@ -1054,6 +1054,47 @@ __global__ void k_larft(int nref, const double* __restrict__ S, const double* __
     for (int idx = threadIdx.x; idx < BT_NB * BT_NB; idx += blockDim.x) Tb[idx] = sT[idx];
 }
 
+// small n (<= 128): apply the reflectors directly, warp per eigenvector
+// (v_j from V in L2, dot by shuffles), then the sign fix and the output copy:
+// one launch instead of larft + 4 GEMMs per 128-reflector block
+__global__ void k_backtransform_small(int n, int nvec, const double* __restrict__ V, const double* __restrict__ tau,
+                                      const double* __restrict__ Z, double* __restrict__ A, int lda) {
+    extern __shared__ double zb[];  // per warp: n
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int q = blockIdx.x * nw + warp;
+    if (q >= nvec) return;
+    double* z = zb + (size_t)warp * n;
+    for (int i = lane; i < n; i += 32) z[i] = Z[(int64_t)i * nvec + q];
+    __syncwarp();
+    for (int j = n - 2; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const double* v = V + (int64_t)j * n;
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], z[i], s);
+        s = warp_sum_d(s) * tj;
+        for (int i = j + 1 + lane; i < n; i += 32) z[i] -= s * v[i];
+        __syncwarp();
+    }
+    double best = -1.0;
+    int at = n;
+    for (int i = lane; i < n; i += 32)
+        if (fabs(z[i]) > best) {
+            best = fabs(z[i]);
+            at = i;
+        }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, at, o);
+        if (ob > best || (ob == best && oa < at)) {
+            best = ob;
+            at = oa;
+        }
+    }
+    const double sg = (z[at] < 0.0) ? -1.0 : 1.0;
+    for (int i = lane; i < n; i += 32) A[i + (int64_t)q * lda] = sg * z[i];
+}
+
 struct Work {
     DeviceBuf V, W, vec, Z, Dp, L, Y, S, T, M1, M2, ws;
     unsigned* bar = nullptr;
@@ -1228,6 +1269,13 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     note_launch();
     k_cluster_orth<<<nvec, 256, sizeof(double) * (size_t)n, st>>>(n, nvec, w, bounds, wk.Z.p);
     AERO_LAUNCHED();
+    if (n <= 128) {  // direct reflector application + sign fix, warp per vector
+        note_launch();
+        k_backtransform_small<<<(nvec + 7) / 8, 256, sizeof(double) * 8 * (size_t)n, st>>>(n, nvec, wk.V.p, tau,
+                                                                                          wk.Z.p, A, lda);
+        AERO_LAUNCHED();
+        return;
+    }
     // Y = columns; then back-transform Y <- Q Y, Q = H_0 ... H_{n-2}
     const int ldy = (n + 1) & ~1;
     wk.Y.alloc((size_t)ldy * nvec);
