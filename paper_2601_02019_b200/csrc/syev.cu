@@ -672,42 +672,32 @@ __device__ __forceinline__ int sturm_count(int s, int t, const double* d, const 
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
     for (int i = s + 1; i < t; ++i) {
-        q = d[i] - x - e2[i - 1] / q;
+        q = d[i] - x - e2[i - 1] * __drcp_rn(q);  // correctly rounded reciprocal: 1 ulp from e2 / q
         if (fabs(q) < pivmin) q = -pivmin;
         cnt += q < 0.0;
     }
     return cnt;
 }
 
-// lower end of the bisection interval of the kc-th smallest eigenvalue of the
-// whole (split) T -> bounds[4]; eigenvalues certainly below it are not needed
-// when only the top n - kc are (one warp, 33-way multisection)
-__global__ void k_cut(int n, int kc, const double* __restrict__ d, const double* __restrict__ e2,
-                      double* __restrict__ bounds) {
-    const int lane = threadIdx.x & 31;
-    const double pivmin = bounds[2];
-    double lo = bounds[0], hi = bounds[1];
-    for (int round = 0; round < 64; ++round) {
-        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
-        if (hi - lo <= tol) break;
-        const double h = (hi - lo) / 33.0;
-        const double x = fmin(lo + h * (lane + 1), hi);
-        const int c = sturm_count(0, n, d, e2, x, pivmin);
-        const unsigned above = __ballot_sync(0xffffffffu, c > kc);
-        double nlo = lo, nhi = hi;
-        if (above) {
-            const int f = __ffs(above) - 1;
-            nhi = __shfl_sync(0xffffffffu, x, f);
-            const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
-            if (f > 0) nlo = xp;
-        } else {
-            nlo = __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (nlo == lo && nhi == hi) break;
-        lo = nlo;
-        hi = nhi;
+// coarse cut: the largest of 1023 evenly spaced points x with global count(x)
+// <= kc (a lower bound of the kc-th smallest eigenvalue) -> bounds[4]; one
+// Sturm sequence per thread, all in parallel
+__global__ void __launch_bounds__(1024) k_cut_coarse(int n, int kc, const double* __restrict__ d,
+                                                     const double* __restrict__ e2, double* __restrict__ bounds) {
+    __shared__ int best[32];
+    const double lo = bounds[0], hi = bounds[1], pivmin = bounds[2];
+    const int m = threadIdx.x;
+    const double x = lo + (hi - lo) * (double)(m + 1) / 1024.0;
+    const int c = (m < 1023) ? sturm_count(0, n, d, e2, x, pivmin) : n;
+    int cand = (c <= kc) ? m : -1;
+    for (int o = 16; o > 0; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+    if ((threadIdx.x & 31) == 0) best[threadIdx.x >> 5] = cand;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int bm = -1;
+        for (int w = 0; w < 32; ++w) bm = max(bm, best[w]);
+        bounds[4] = (bm < 0) ? lo : lo + (hi - lo) * (double)(bm + 1) / 1024.0;
     }
-    if (lane == 0) bounds[4] = lo - 2.0 * DBL_EPSILON * fabs(lo) - pivmin;
 }
 
 // one warp per row p: the (p - s)-th smallest eigenvalue of p's block [s, t),
@@ -906,38 +896,59 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
         }
         return;
     }
-    // bottom-up: D-(i) into Z, twist index by min |gamma|
+    // bottom-up: D-(i) into Z, twist index by min |gamma|. The loads that do
+    // not depend on the recurrence are issued 8 ahead (global scratch is L2).
+    constexpr int PF = 8;
     double dm = safe(sd[bt - 1] - lv);
     ZZ(bt - 1) = dm;
     int r = bt - 1;
     double best = fabs(dp);  // gamma at the last row = D+(last)
-#pragma unroll 4
-    for (int i = bt - 2; i >= bs; --i) {
-        const double dpi = DP(i);
-        dm = safe(sd[i] - lv - se[i] * (se[i] / dm));
-        ZZ(i) = dm;
-        const double g = dpi + dm - (sd[i] - lv);
-        if (fabs(g) < best) {
-            best = fabs(g);
-            r = i;
+    for (int ib = bt - 2; ib >= bs; ib -= PF) {
+        double pre[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) pre[u] = (ib - u >= bs) ? DP(ib - u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = ib - u;
+            if (i < bs) break;
+            dm = safe(sd[i] - lv - se[i] * (se[i] / dm));
+            ZZ(i) = dm;
+            const double g = pre[u] + dm - (sd[i] - lv);
+            if (fabs(g) < best) {
+                best = fabs(g);
+                r = i;
+            }
         }
     }
     // solve outward from r
     double nrm2 = 1.0, z = 1.0;
-#pragma unroll 4
-    for (int i = r; i < bt - 1; ++i) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
-        const double dmn = ZZ(i + 1);
-        z = -(se[i] / dmn) * z;
-        ZZ(i + 1) = z;
-        nrm2 += z * z;
+    for (int ib = r; ib < bt - 1; ib += PF) {  // z_{i+1} = -(e_i / D-(i+1)) z_i
+        double pre[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) pre[u] = (ib + u < bt - 1) ? ZZ(ib + u + 1) : 1.0;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = ib + u;
+            if (i >= bt - 1) break;
+            z = -(se[i] / pre[u]) * z;
+            ZZ(i + 1) = z;
+            nrm2 += z * z;
+        }
     }
     ZZ(r) = 1.0;
     z = 1.0;
-#pragma unroll 4
-    for (int i = r - 1; i >= bs; --i) {  // z_i = -(e_i / D+(i)) z_{i+1}
-        z = -(se[i] / DP(i)) * z;
-        ZZ(i) = z;
-        nrm2 += z * z;
+    for (int ib = r - 1; ib >= bs; ib -= PF) {  // z_i = -(e_i / D+(i)) z_{i+1}
+        double pre[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) pre[u] = (ib - u >= bs) ? DP(ib - u) : 1.0;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+            const int i = ib - u;
+            if (i < bs) break;
+            z = -(se[i] / pre[u]) * z;
+            ZZ(i) = z;
+            nrm2 += z * z;
+        }
     }
     const double sc = 1.0 / sqrt(nrm2);
 #pragma unroll 4
@@ -1237,9 +1248,9 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     AERO_LAUNCHED();
     const size_t sde = 2 * sizeof(double) * (size_t)n;
     note_launch();
-    if (nvec < n - 1 && n >= 512) {  // only the top nvec + 1 eigenvalues are needed
+    if (nvec < n - 1 && n >= 256) {  // only the top nvec + 1 eigenvalues are needed
         note_launch();
-        k_cut<<<1, 32, 0, st>>>(n, n - nvec - 1, d, e2, bounds);
+        k_cut_coarse<<<1, 1024, 0, st>>>(n, n - nvec - 1, d, e2, bounds);
         AERO_LAUNCHED();
     } else {
         const double ninf = -DBL_MAX;
@@ -1257,9 +1268,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     note_launch();
     wk.L.alloc((size_t)3 * n * nvec);
     {  // per-thread scratch in shared memory when 2 n x threads doubles fit
-        int tb = 32;
-        while (tb > 4 && sde + 2 * sizeof(double) * (size_t)n * tb > 200 * 1024) tb /= 2;
-        const bool usm = sde + 2 * sizeof(double) * (size_t)n * tb <= 200 * 1024;
+        const int tb = 32;
+        const bool usm = sde + 2 * sizeof(double) * (size_t)n * tb <= 200 * 1024;  // else L2 scratch, prefetched
         const size_t sm_tw = sde + (usm ? 2 * sizeof(double) * (size_t)n * tb : 0);
         k_twisted<<<(nvec + tb - 1) / tb, tb, sm_tw, st>>>(n, nvec, d, e, lam, w, order, blk, bounds, wk.Dp.p,
                                                           wk.L.p, wk.L.p + (size_t)n * nvec,
