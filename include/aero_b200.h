@@ -229,6 +229,16 @@ int64_t aero_kernel_launches(void);
  * w descending, v columns = eigenvectors sign-fixed; device_ms (nullable)
  * receives the device time of the solve */
 int aero_eigh(int32_t n, const double* a, double* w, double* v, double* device_ms);
+/* The iteration product Y = G X (test hook): mode 0 = int8 tensor cores by
+ * exact slicing (ozaki.cu), mode 1 = fp64 DMMA (product.cu). g is r x r symmetric, x is r x n column-major
+ * (column j = x + j*r), colmask (nullable) gives each column's prefix length
+ * (entries of x at k >= colmask[j] are treated as 0; output rows i >=
+ * colmask[j] are 0); y is r x n column-major; device_ms (nullable) receives
+ * the mean device time of one product over 20 launches after a warm-up
+ * (mode 0: slicing of x, MMA and split-K sum; the slicing of g is done once
+ * before, as the engine does once per batch). */
+int aero_dev_product(int32_t r, int32_t n, const double* g, const double* x, const int32_t* colmask,
+                     int32_t mode, double* y, double* device_ms);
 /* RngState draws on the device (test hook): count gaussians of fork #fork of
  * RngState(seed, stream) (fork 0 = the root), to host memory */
 int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out);

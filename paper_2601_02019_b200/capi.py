@@ -158,6 +158,7 @@ SIGNATURES = [
     ("aero_kernel_launches", i64, []),
     ("aero_rng_gaussians", i32, [u64, u64, i64, i64, P(f64)]),
     ("aero_eigh", i32, [i32, P(f64), P(f64), P(f64), P(f64)]),
+    ("aero_dev_product", i32, [i32, i32, P(f64), P(f64), P(i32), i32, P(f64), P(f64)]),
 ]
 
 _lib = None
@@ -212,6 +213,23 @@ def eigh(b, return_ms=False):
     w, v, ms = np.empty(n), np.empty((n, n)), f64()
     _chk(lib().aero_eigh(n, _dp(b), _dp(w), _dp(v), C.byref(ms)))
     return (w, v, ms.value) if return_ms else (w, v)
+
+
+def dev_product(g, x, colmask=None, mode=0, return_ms=False):
+    """Y = G X through the engine's product kernels (test hook): mode 0 = int8
+    tensor cores by exact slicing (ozaki.cu), 1 = fp64 DMMA (product.cu).
+    g: r x r symmetric; x: r x n; colmask: per-column prefix lengths."""
+    g = _f64(g)
+    r, n = g.shape[0], x.shape[1]
+    xt = np.ascontiguousarray(np.asarray(x, dtype=np.float64).T)  # column-major r x n
+    y = np.empty((n, r))
+    ms = f64()
+    cm = None
+    if colmask is not None:
+        cm = np.ascontiguousarray(colmask, dtype=np.int32)
+    _chk(lib().aero_dev_product(r, n, _dp(g), _dp(xt), cm.ctypes.data_as(P(i32)) if cm is not None else None,
+                                mode, _dp(y), C.byref(ms) if return_ms else None))
+    return (y.T, ms.value) if return_ms else y.T
 
 
 def _device_ptr(x):

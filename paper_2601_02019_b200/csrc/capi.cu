@@ -180,6 +180,87 @@ int aero_reset_profile(aero_sketch* h) {
     return AERO_OK;
 }
 
+int aero_dev_product(int32_t r, int32_t n, const double* g, const double* x, const int32_t* colmask,
+                     int32_t mode, double* y, double* device_ms) {
+    REQ(g);
+    REQ(x);
+    REQ(y);
+    return guard([&] {
+        if (r < 1 || n < 1) throw InvalidInput("product: empty input");
+        if (mode != 0 && mode != 1) throw InvalidInput("product: mode must be 0 or 1");
+        const int ld = r + (r & 1);
+        double *dG, *dX, *dY, *dW;
+        int* dM = nullptr;
+        const size_t wsn = product_workspace_doubles(r, n);
+        AERO_CUDA(cudaMalloc(&dG, sizeof(double) * (size_t)ld * r));
+        AERO_CUDA(cudaMalloc(&dX, sizeof(double) * (size_t)ld * n));
+        AERO_CUDA(cudaMalloc(&dY, sizeof(double) * (size_t)ld * n));
+        AERO_CUDA(cudaMalloc(&dW, sizeof(double) * wsn));
+        AERO_CUDA(cudaMemcpy2D(dG, sizeof(double) * ld, g, sizeof(double) * r, sizeof(double) * r, r,
+                               cudaMemcpyHostToDevice));
+        AERO_CUDA(cudaMemcpy2D(dX, sizeof(double) * ld, x, sizeof(double) * r, sizeof(double) * r, n,
+                               cudaMemcpyHostToDevice));
+        if (colmask) {
+            AERO_CUDA(cudaMalloc(&dM, sizeof(int) * n));
+            AERO_CUDA(cudaMemcpy(dM, colmask, sizeof(int) * n, cudaMemcpyHostToDevice));
+        }
+        OzakiGram oz;
+        cudaStream_t st = 0;
+        if (mode == 0) oz.prepare(st, r, dG, ld);
+        static const bool dbg_on = getenv("AERO_OZAKI_DEBUG") != nullptr;  // dev: per-CTA phase stamps
+        unsigned long long* dbg = nullptr;
+        if (dbg_on && mode == 0) {
+            AERO_CUDA(cudaMalloc(&dbg, 8 * 8 * 4096));
+            AERO_CUDA(cudaMemset(dbg, 0, 8 * 8 * 4096));
+            oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn);
+            oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn, dbg);
+            std::vector<unsigned long long> h(8 * 4096);
+            AERO_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+            unsigned long long t0 = ~0ull, tend = 0;
+            double acc[7] = {0};
+            int nc = 0;
+            for (int c = 0; c < 4096 && h[c * 8]; ++c, ++nc) {
+                t0 = std::min(t0, h[c * 8]);
+                tend = std::max(tend, h[c * 8 + 6]);
+                for (int k = 1; k < 7; ++k)
+                    if (h[c * 8 + k]) acc[k] += (double)(h[c * 8 + k] - h[c * 8 + k - 1]);
+            }
+            fprintf(stderr, "ozaki r=%d n=%d ctas=%d span %.2f us; mean us: alloc %.2f first-load %.2f mma %.2f epi-wait %.2f epi %.2f end %.2f\n",
+                    r, n, nc, (tend - t0) / 1e3, acc[1] / nc / 1e3, acc[2] / nc / 1e3, acc[3] / nc / 1e3,
+                    acc[4] / nc / 1e3, acc[5] / nc / 1e3, acc[6] / nc / 1e3);
+            cudaFree(dbg);
+        }
+        auto run = [&] {
+            if (mode == 0) oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn);
+            else gemm_product(st, r, n, r, dG, ld, dX, ld, dY, ld, dM, dW, wsn);
+        };
+        run();
+        AERO_CUDA(cudaStreamSynchronize(st));
+        AERO_CUDA(cudaMemcpy2D(y, sizeof(double) * r, dY, sizeof(double) * ld, sizeof(double) * r, n,
+                               cudaMemcpyDeviceToHost));
+        if (device_ms) {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, st);
+            for (int it = 0; it < 20; ++it) run();
+            cudaEventRecord(e1, st);
+            AERO_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            *device_ms = ms / 20.0;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        oz.release();
+        cudaFree(dG);
+        cudaFree(dX);
+        cudaFree(dY);
+        cudaFree(dW);
+        if (dM) cudaFree(dM);
+    });
+}
+
 int aero_eigh(int32_t n, const double* a, double* w, double* v, double* device_ms) {
     REQ(a);
     REQ(w);

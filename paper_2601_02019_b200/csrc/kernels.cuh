@@ -34,6 +34,25 @@ void gemm_acc(cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alp
 void gemm_product(cudaStream_t st, int M, int N, int K, const double* A, int lda, const double* B,
                   int ldb, double* Y, int ldy, const int* colmask, double* ws, size_t ws_doubles);
 
+// Y = G X (fp64 in and out) on the int8 tensor cores by exact slicing
+// (Ozaki scheme, ozaki.cu). prepare() slices G (r x r, symmetric, column i =
+// row i at G + i*ldg) once per Gram; product() slices X (R x N, column j
+// masked to rows < colmask[j]) and runs the tcgen05 kind::i8 kernel; output
+// rows i >= colmask[j] of column j are 0. Split-K partials go through ws.
+struct OzakiGram {
+    int R = 0, Rp = 0, Kp = 0;
+    int8_t *a = nullptr, *b = nullptr;
+    int *ea = nullptr, *fb = nullptr;
+    size_t a_bytes = 0, b_bytes = 0, ea_n = 0, fb_n = 0;
+    void prepare(cudaStream_t st, int R, const double* G, int ldg);
+    // dbg (dev instrumentation, nullable): 8 globaltimer stamps per CTA
+    void product(cudaStream_t st, int N, const double* X, int ldx, const int* colmask, double* Y, int ldy,
+                 double* ws, size_t ws_doubles, unsigned long long* dbg = nullptr);
+    void release();
+    ~OzakiGram() { release(); }
+};
+int ozaki_slices();
+
 // per-row squared norm and finiteness of n rows (row-major, ld) -> nrm2[n], bad[n]
 void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int d, double* nrm2,
                  int* bad);

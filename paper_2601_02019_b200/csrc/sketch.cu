@@ -323,6 +323,9 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     } else {
     if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
     iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+    // large buffers: G sliced once for all phases, products on the int8 tensor cores
+    const bool i8 = i8_ && R >= i8_min_rows_;
+    if (i8) oz_.prepare(st_, R, G_.p, cap_);
     for (int p = 0; p < maxphase; ++p) {
         int ncol = 0;
         double flops = 0.0;
@@ -336,11 +339,16 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         // one CTA per job streams all partials -- profiles/round1_c2_steady_launches.txt)
         constexpr bool kFuseSplitK = false;
         int splits = 1;
-        const bool fast = gemm_big(st_, false, false, R, ncol, R, G_.p, cap_, X_.p, ldx_, Y_.p,
-                                   ldx_, colmask_d_, ws_.p, ws_.n, &splits, kFuseSplitK && max_k <= 4);
-        if (!fast)
-            dgemm(st_, false, false, R, ncol, R, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_,
-                  colmask_d_);
+        bool fast = true;
+        if (i8) {
+            oz_.product(st_, ncol, X_.p, ldx_, colmask_d_, Y_.p, ldx_, ws_.p, ws_.n);
+        } else {
+            fast = gemm_big(st_, false, false, R, ncol, R, G_.p, cap_, X_.p, ldx_, Y_.p, ldx_, colmask_d_,
+                            ws_.p, ws_.n, &splits, kFuseSplitK && max_k <= 4);
+            if (!fast)
+                dgemm(st_, false, false, R, ncol, R, 1.0, G_.p, cap_, X_.p, ldx_, 0.0, Y_.p, ldx_,
+                      colmask_d_);
+        }
         if (profiling) {
             AERO_CUDA(cudaEventRecord(ev_at(3 + 2 * p), st_));
             prof.product_launches++;

@@ -134,6 +134,13 @@ class Sketch {
     int* phase_h_ = nullptr;
     unsigned* bar_d_ = nullptr;  // grid-barrier counter of the persistent iterate
     bool persistent_ = getenv("AERO_NO_PERSISTENT") == nullptr;  // dev A/B switch
+    // iteration products of large buffers on the int8 tensor cores (ozaki.cu);
+    // AERO_PRODUCT_I8=0 keeps them on fp64 DMMA (dev A/B switch)
+    bool i8_ = !(getenv("AERO_PRODUCT_I8") && getenv("AERO_PRODUCT_I8")[0] == '0');
+    // buffer rows from which it is used (tools/product_i8_bench.py: at r = 1500,
+    // n = 128..192 it beats DMMA); AERO_I8_MIN_ROWS overrides (tests force it on)
+    int i8_min_rows_ = getenv("AERO_I8_MIN_ROWS") ? atoi(getenv("AERO_I8_MIN_ROWS")) : 1024;
+    OzakiGram oz_;
     int* status_d_ = nullptr;
     int* clamp_d_ = nullptr;
     int* colmask_d_ = nullptr;

@@ -258,6 +258,35 @@ def test_persistent_iterate_matches_launch_sequence(orc, monkeypatch):
     assert_trace_equal(ev_a, ref.update_block(rows, ts))
 
 
+@pytest.mark.parametrize("cfg", ["c1", "ell128", "ell512"])
+def test_int8_tensor_product_iterate_parity(orc, monkeypatch, cfg):
+    """The iteration products on the int8 tensor cores (ozaki.cu), forced on
+    for every buffer size (AERO_I8_MIN_ROWS=1; per-phase launch sequence),
+    keep the decision trace identical to the oracle's and the sketch within
+    the fp64 tolerances."""
+    monkeypatch.setenv("AERO_NO_PERSISTENT", "1")
+    monkeypatch.setenv("AERO_I8_MIN_ROWS", "1")
+    if cfg == "c1":
+        d, eps, seed, n = 1024, 1 / 16, 1, 900
+        rows = c1_rows(orc, n)
+    elif cfg == "ell128":
+        d, eps, seed, n = 256, 1 / 64, 4, 700
+        rows = orc.gen_rows(d, 48, 0.97, 0.05, 32.0, 4, 0, 1, n)
+    else:
+        d, eps, seed, n = 1024, 1 / 256, 6, 1300
+        orc.set_threads(8)
+        rows = orc.gen_rows(d, 64, 0.97, 0.05, 64.0, 6, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, eps, seed, 1000)
+    ev_ref = ref.update_block(rows, ts)
+    orc.set_threads(1)
+    s = prod.AttpState(d, eps, seed=seed, stream=1000)
+    ev = s.update_block(rows, ts)
+    assert ev_ref["gate_fired"].sum() > 0
+    assert_trace_equal(ev, ev_ref, rtol=1e-7)
+    assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-8
+
+
 # ---------------------------------------------------------------- sliding window
 @pytest.mark.parametrize("n_win,scale_rows", [(500, ()), (50, (100, 700, 1200))])
 def test_ml_bookkeeping_bit_exact(orc, n_win, scale_rows):
@@ -473,3 +502,53 @@ def test_distributed_sketch_nccl_merge(orc):
     assert ds.exchange.mass_bytes + ds.snapshot_bytes == ref["comm_bytes"]
     assert np.max(np.abs(np.array(errs) - ref["probe_err"])) <= 1e-6
     assert rel_fro(gram, ref["last_probe_gram"]) < 1e-9
+
+
+def _product_case(r, n, seed, spread=4.0):
+    """PSD Gram with rows of very different scale (reduced rows ~1e4, new rows
+    ~1) and masked job columns, like the iterate product at C2."""
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((r, max(8, r // 2))) * np.exp(spread * rng.random((r, 1)))
+    g = a @ a.T
+    x = rng.standard_normal((r, n))
+    mask = rng.integers(max(1, r - 70), r + 1, size=n).astype(np.int32)
+    mask[0] = r
+    for j in range(n):
+        x[mask[j]:, j] = 0.0
+    return g, x, mask
+
+
+def _product_ref(g, x, mask):
+    y = np.zeros_like(x)
+    bound = np.zeros_like(x)
+    for j in range(x.shape[1]):
+        m = mask[j]
+        y[:m, j] = g[:m, :m] @ x[:m, j]
+        bound[:m, j] = np.abs(g[:m, :m]) @ np.abs(x[:m, j])
+    return y, bound
+
+
+@pytest.mark.parametrize("r,n", [(64, 1), (129, 3), (700, 64), (1500, 130), (2047, 192)])
+def test_int8_tensor_product_matches_fp64(r, n):
+    """ozaki.cu (tcgen05 kind::i8, 7 slices of 7 bits) vs numpy fp64.
+    Tolerance = the scheme's bound: row i of G and column c of X are cut
+    relative to their largest entries, so each product term is exact to
+    2^-46 max_k|G_ik| max_k|X_kc| and an entry to m_c 2^-44 max|G_i| max|X_c|
+    (m_c = the column's prefix length). The fp64 DMMA path is held to the fp64
+    GEMM componentwise bound 1e-13 |G||X| (K u = 4.5e-13 at K = 2047).
+    Masked rows are exactly 0 on both paths."""
+    g, x, mask = _product_case(r, n, seed=r + n)
+    y_ref, bound = _product_ref(g, x, mask)
+    for mode in (0, 1):
+        y = prod.dev_product(g, x, mask, mode=mode)
+        err = np.abs(y - y_ref)
+        if mode == 0:
+            tol = np.zeros_like(x)
+            for j in range(n):
+                m = mask[j]
+                tol[:m, j] = m * 2.0**-44 * np.max(np.abs(g[:m, :m]), axis=1) * np.max(np.abs(x[:m, j]))
+        else:
+            tol = 1e-13 * bound
+        assert np.all(err <= tol + 1e-300), (mode, float(np.max(err / np.maximum(tol, 1e-300))))
+        for j in range(n):
+            assert np.all(y[mask[j]:, j] == 0.0)
