@@ -35,13 +35,14 @@
 
 #include "aero_common.cuh"
 #include "kernels.cuh"
+#include "ozaki.cuh"
 
 namespace aero_b200 {
 
 namespace {
-constexpr int OZ_BM = 128;  // rows of G per CTA (UMMA M)
-constexpr int OZ_BN = 64;   // job columns per CTA (UMMA N)
-constexpr int OZ_BK = 64;   // K bytes (int8 elements) per stage
+constexpr int OZ_BM = kOzBM;  // rows of G per CTA (UMMA M)
+constexpr int OZ_BN = kOzBN;  // job columns per CTA (UMMA N)
+constexpr int OZ_BK = kOzBK;  // K bytes (int8 elements) per stage
 constexpr int OZ_THREADS = 256;
 
 template <int S>
@@ -130,56 +131,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 }
 
 // Slices of `nvec` fp64 vectors of length K (vector i at V + i*ldv; entries
-// at k >= lim_i are zero, lim_i = min(mask[i], K) or K) in the tiled image the
-// product kernel copies: tiles of TR vectors; block (tile t, K block b) at
-// out + (t * nkb + b) * S * TR * 64 holds slice p at p * TR * 64, vector row
-// r at 64 r, its 16-byte chunk c at chunk c ^ ((r >> 1) & 3). Vectors
-// nvec.. of the last tile and k in [lim_i, Kp) are zero. One CTA per vector;
-// ex[i] = the vector's scale exponent.
+// at k >= lim_i are zero, lim_i = min(mask[i], K) or K) into the tiled image
+// (ozaki.cuh); vectors nvec.. of the last tile are zero. One CTA per vector.
 constexpr int SL_THREADS = 256;
 template <int S, int TR>
 __global__ void __launch_bounds__(SL_THREADS) k_ozaki_slice(int nvec, int K, int Kp, const double* __restrict__ V,
                                                             int ldv, const int* __restrict__ mask,
                                                             int8_t* __restrict__ out, int* __restrict__ ex) {
     __shared__ double red[SL_THREADS / 32];
-    const int i = blockIdx.x, tid = threadIdx.x;
+    const int i = blockIdx.x;
     int lim = 0;
     if (i < nvec) lim = mask ? min(mask[i], K) : K;
-    const double* v = V + (int64_t)i * ldv;
-    double m = 0.0;
-#pragma unroll 8
-    for (int k = tid; k < lim; k += SL_THREADS) m = fmax(m, fabs(__ldg(v + k)));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) red[tid >> 5] = m;
-    __syncthreads();
-    m = 0.0;
-#pragma unroll
-    for (int w = 0; w < SL_THREADS / 32; ++w) m = fmax(m, red[w]);
-    const int e = (m > 0.0) ? ilogb(m) + 1 : 0;  // |v| < 2^e
-    if (tid == 0) ex[i] = e;
-    const int nkb = Kp / OZ_BK, t = i / TR, r = i % TR;
-    for (int k0 = tid * 8; k0 < Kp; k0 += SL_THREADS * 8) {
-        double x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = (k0 + u < lim) ? scalbn(__ldg(v + k0 + u), 7 - e) : 0.0;  // |x| < 128
-        uint64_t pk[S];
-#pragma unroll
-        for (int p = 0; p < S; ++p) pk[p] = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-#pragma unroll
-            for (int p = 0; p < S; ++p) {
-                const double sv = trunc(x[u]);
-                x[u] = (x[u] - sv) * 128.0;
-                pk[p] |= (uint64_t)(uint8_t)(int8_t)(int)sv << (8 * u);
-            }
-        }
-        const int b = k0 / OZ_BK, kk = k0 % OZ_BK, kc = kk >> 4;
-        int8_t* blk = out + ((int64_t)t * nkb + b) * S * TR * OZ_BK + r * OZ_BK + ((kc ^ ((r >> 1) & 3)) << 4) + (kk & 15);
-#pragma unroll
-        for (int p = 0; p < S; ++p) *reinterpret_cast<uint64_t*>(blk + p * TR * OZ_BK) = pk[p];
-    }
+    ozaki_slice_vector<S, TR>(V + (int64_t)i * ldv, lim, Kp, i, out, ex, red);
 }
 
 template <int S>
@@ -339,7 +302,7 @@ __global__ void k_ozaki_reduce(int M, int N, int splits, const double* __restric
     Y[i + (int64_t)j * ldy] = v;
 }
 
-constexpr int kSlices = 7;
+constexpr int kSlices = kOzSlices;
 }  // namespace
 
 int ozaki_slices() { return kSlices; }
