@@ -207,29 +207,6 @@ int aero_dev_product(int32_t r, int32_t n, const double* g, const double* x, con
         OzakiGram oz;
         cudaStream_t st = 0;
         if (mode == 0) oz.prepare(st, r, dG, ld);
-        static const bool dbg_on = getenv("AERO_OZAKI_DEBUG") != nullptr;  // dev: per-CTA phase stamps
-        unsigned long long* dbg = nullptr;
-        if (dbg_on && mode == 0) {
-            AERO_CUDA(cudaMalloc(&dbg, 8 * 8 * 4096));
-            AERO_CUDA(cudaMemset(dbg, 0, 8 * 8 * 4096));
-            oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn);
-            oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn, dbg);
-            std::vector<unsigned long long> h(8 * 4096);
-            AERO_CUDA(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
-            unsigned long long t0 = ~0ull, tend = 0;
-            double acc[7] = {0};
-            int nc = 0;
-            for (int c = 0; c < 4096 && h[c * 8]; ++c, ++nc) {
-                t0 = std::min(t0, h[c * 8]);
-                tend = std::max(tend, h[c * 8 + 6]);
-                for (int k = 1; k < 7; ++k)
-                    if (h[c * 8 + k]) acc[k] += (double)(h[c * 8 + k] - h[c * 8 + k - 1]);
-            }
-            fprintf(stderr, "ozaki r=%d n=%d ctas=%d span %.2f us; mean us: alloc %.2f first-load %.2f mma %.2f epi-wait %.2f epi %.2f end %.2f\n",
-                    r, n, nc, (tend - t0) / 1e3, acc[1] / nc / 1e3, acc[2] / nc / 1e3, acc[3] / nc / 1e3,
-                    acc[4] / nc / 1e3, acc[5] / nc / 1e3, acc[6] / nc / 1e3);
-            cudaFree(dbg);
-        }
         auto run = [&] {
             if (mode == 0) oz.product(st, n, dX, ld, dM, dY, ld, dW, wsn);
             else gemm_product(st, r, n, r, dG, ld, dX, ld, dY, ld, dM, dW, wsn);

@@ -6,6 +6,7 @@
 
 #include "aero_common.cuh"
 #include "kernels.cuh"
+#include "ozaki.cuh"
 #include "tiles.cuh"
 
 namespace aero_b200 {
@@ -396,17 +397,26 @@ __device__ void cta_gram(const double* P, int ldp, const double* Q, int ldq, int
         double part[KM * KM];
 #pragma unroll
         for (int e = 0; e < KM * KM; ++e) part[e] = 0.0;
-        for (int i = tid; i < r; i += nt) {
-            double p[KM], q[KM];
+        // RU rows per thread per round: all their loads in flight before the
+        // FMAs (one L2 round trip per round instead of one per row)
+        constexpr int RU = (KM <= 16) ? 16 / KM : 1;
+        for (int i0 = tid; i0 < r; i0 += RU * nt) {
+            double p[RU][KM], q[RU][KM];
 #pragma unroll
-            for (int a = 0; a < KM; ++a) {
-                p[a] = (a < k) ? P[i + (int64_t)a * ldp] : 0.0;
-                q[a] = (a < k) ? Q[i + (int64_t)a * ldq] : 0.0;
+            for (int u = 0; u < RU; ++u) {
+                const int i = i0 + u * nt;
+#pragma unroll
+                for (int a = 0; a < KM; ++a) {
+                    p[u][a] = (i < r && a < k) ? P[i + (int64_t)a * ldp] : 0.0;
+                    q[u][a] = (i < r && a < k) ? Q[i + (int64_t)a * ldq] : 0.0;
+                }
             }
 #pragma unroll
-            for (int a = 0; a < KM; ++a)
+            for (int u = 0; u < RU; ++u)
 #pragma unroll
-                for (int b = 0; b < KM; ++b) part[a + b * KM] = fma(p[a], q[b], part[a + b * KM]);
+                for (int a = 0; a < KM; ++a)
+#pragma unroll
+                    for (int b = 0; b < KM; ++b) part[a + b * KM] = fma(p[u][a], q[u][b], part[a + b * KM]);
         }
         const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
 #pragma unroll
@@ -505,12 +515,34 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     const double* y;
     int ldy;
     if (WS) {
-        for (int e = tid; e < r * k; e += nt) {
-            const int i = e % r, a = e / r;
-            const double* p = ws + i + (int64_t)(jb.col + a) * wsM;
-            double v = 0.0;
-            for (int z = 0; z < splits; ++z) v += __ldcg(p + z * sstride);
-            ysh[e] = v;
+        // fixed-order split-K sum; 8 entries x 4 splits of loads in flight per
+        // thread (a plain per-entry loop serializes one L2 round trip per split)
+        constexpr int U = 8;
+        const int tot = r * k;
+        for (int e0 = tid; e0 < tot; e0 += U * nt) {
+            const double* pp[U];
+            bool ok[U];
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * nt;
+                ok[u] = e < tot;
+                const int ee = ok[u] ? e : 0;
+                pp[u] = ws + ee % r + (int64_t)(jb.col + ee / r) * wsM;
+                v[u] = 0.0;
+            }
+            for (int z = 0; z < splits; z += 4) {
+                double t[U][4];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) t[u][q] = (ok[u] && z + q < splits) ? __ldcg(pp[u] + (z + q) * sstride) : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] += (t[u][0] + t[u][1]) + (t[u][2] + t[u][3]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (ok[u]) ysh[e0 + u * nt] = v[u];
         }
         __syncthreads();
         y = ysh;
@@ -562,29 +594,42 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     __syncthreads();
     for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
     __syncthreads();
-    // rows independent: [last: H = X T], X <- Y T
-    for (int i = tid; i < r; i += nt) {
-        double xr[KM], yr[KM];
+    // rows independent: [last: H = X T], X <- Y T; RU rows per thread per
+    // round with all their loads issued first (one L2 round trip per round)
+    {
+        constexpr int RU = (KM <= 4) ? 16 / KM : 1;
+        for (int i0 = tid; i0 < r; i0 += RU * nt) {
+            double xr[RU][KM], yr[RU][KM];
 #pragma unroll
-        for (int a = 0; a < KM; ++a) {
-            if (a < k) {
-                xr[a] = x[i + (int64_t)a * ldx];
-                yr[a] = y[i + (int64_t)a * ldy];
-            }
-        }
+            for (int u = 0; u < RU; ++u) {
+                const int i = i0 + u * nt;
 #pragma unroll
-        for (int b = 0; b < KM; ++b) {
-            if (b >= k) break;
-            double hx = 0.0, hy = 0.0;
-#pragma unroll
-            for (int a = 0; a < KM; ++a) {
-                if (a < k) {
-                    hx = fma(xr[a], T[a + b * k], hx);
-                    hy = fma(yr[a], T[a + b * k], hy);
+                for (int a = 0; a < KM; ++a) {
+                    if (a < k && i < r) {
+                        xr[u][a] = x[i + (int64_t)a * ldx];
+                        yr[u][a] = y[i + (int64_t)a * ldy];
+                    }
                 }
             }
-            if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;
-            x[i + (int64_t)b * ldx] = hy;
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int i = i0 + u * nt;
+                if (i >= r) break;
+#pragma unroll
+                for (int b = 0; b < KM; ++b) {
+                    if (b >= k) break;
+                    double hx = 0.0, hy = 0.0;
+#pragma unroll
+                    for (int a = 0; a < KM; ++a) {
+                        if (a < k) {
+                            hx = fma(xr[u][a], T[a + b * k], hx);
+                            hy = fma(yr[u][a], T[a + b * k], hy);
+                        }
+                    }
+                    if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;
+                    x[i + (int64_t)b * ldx] = hy;
+                }
+            }
         }
     }
     __syncthreads();
@@ -674,6 +719,166 @@ __global__ void __launch_bounds__(tiles::PNT, 2) k_iterate(IterPersistArgs a) {
         }
         grid_sync(a.bar, epoch, G);
     }
+}
+
+// ---- persistent iteration with the products on the int8 tensor cores -------
+// phase p: [all CTAs] (tile, split) work items of Y = G X (ozaki_tile, TMEM
+// allocated once per CTA) -> grid barrier -> [CTA per job] fixed-order split-K
+// sum + normalize, then the new iterate columns are sliced for the next
+// product -> grid barrier. Same arithmetic as the per-phase launch sequence
+// (OzakiGram::product + iter_normalize).
+struct IterI8Args {
+    const IterJob* jobs;
+    int njobs, maxphase, R, ldx, kv, Kp, Rp;
+    double *X, *H, *out_sig, *out_vr, *ws;
+    int *status, *out_clamped;
+    const int* colmask;
+    const int* phase_ncol;
+    const int* phase_splits;
+    unsigned* bar;
+    const int8_t* ga;
+    const int* gea;
+    int8_t* xb;
+    int* xfe;
+    unsigned long long* prof;  // optional (AERO_I8_PROF): CTA 0 ns per segment
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int KM>
+__global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+    double* smd = reinterpret_cast<double*>(sm);
+    __shared__ uint32_t slot;
+    constexpr int S = kOzSlices;
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&slot)),
+                     "r"(OzCfg<S>::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = slot;
+    unsigned epoch = 0;
+    const unsigned G = gridDim.x;
+    const int R = a.R, nkb_all = a.Kp / kOzBK, tm = a.Rp / kOzBM;
+    {  // X slices for phase 0
+        const int ncol0 = a.phase_ncol[0], np0 = (ncol0 + kOzBN - 1) / kOzBN * kOzBN;
+        for (int c = blockIdx.x; c < np0; c += G) {
+            const int lim = (c < ncol0) ? min(a.colmask[c], R) : 0;
+            ozaki_slice_vector<S, kOzBN>(a.X + (int64_t)c * a.ldx, lim, a.Kp, c, a.xb, a.xfe, smd);
+            __syncthreads();
+        }
+    }
+    grid_sync(a.bar, epoch, G);
+    const bool pr = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long tp = pr ? gtimer() : 0;
+#define I8_MARK(i)                              \
+    if (pr) {                                   \
+        const unsigned long long t_ = gtimer(); \
+        a.prof[i] += t_ - tp;                   \
+        tp = t_;                                \
+    }
+    for (int p = 0; p < a.maxphase; ++p) {
+        const int ncol = a.phase_ncol[p], splits = a.phase_splits[p];
+        const int tn = (ncol + kOzBN - 1) / kOzBN, per = (nkb_all + splits - 1) / splits;
+        const int items = tn * tm * splits;
+        const int64_t sstride = (int64_t)R * ncol;
+        for (int it = blockIdx.x; it < items; it += G) {
+            const int z = it / (tn * tm), rem = it % (tn * tm);
+            const int kb0 = z * per, nkb = max(0, min(nkb_all - kb0, per));
+            ozaki_tile<S>(R, ncol, nkb_all, rem / tn, rem % tn, kb0, nkb, a.ga, a.xb, a.gea, a.xfe,
+                          a.ws + z * sstride, R, nullptr, 0, sm, tmem);
+        }
+        I8_MARK(0);
+        grid_sync(a.bar, epoch, G);
+        I8_MARK(1);
+        for (int j = blockIdx.x; j < a.njobs; j += G) {
+            const IterJob jb = a.jobs[j];
+            __syncthreads();
+            normalize_job<KM, true>(jb, j, p, a.X, nullptr, a.ldx, a.H, a.status, a.out_sig, a.out_vr, a.kv,
+                                    a.out_clamped, a.ws, R, sstride, splits, smd);
+            __syncthreads();
+            if (j == 0) I8_MARK(4);
+            if (p + 1 < jb.nphase && *(volatile int*)(a.status + j) == JOB_ACTIVE) {
+                if (jb.k == 2)  // both columns in one pass (one shared reduction)
+                    ozaki_slice_vectors<S, kOzBN, 2>(a.X + (int64_t)jb.col * a.ldx, a.ldx, jb.r, a.Kp, jb.col, a.xb,
+                                                     a.xfe, smd);
+                else
+                    for (int c = 0; c < jb.k; ++c)
+                        ozaki_slice_vector<S, kOzBN>(a.X + (int64_t)(jb.col + c) * a.ldx, jb.r, a.Kp, jb.col + c,
+                                                     a.xb, a.xfe, smd);
+            }
+        }
+        I8_MARK(2);
+        grid_sync(a.bar, epoch, G);
+        I8_MARK(3);
+    }
+#undef I8_MARK
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                     "r"(OzCfg<S>::TMEM_COLS));
+    }
+}
+
+int ozaki_splits(const OzakiGram& oz, int N, size_t ws_doubles) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        AERO_CUDA(cudaGetDevice(&dev));
+        AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int tm = oz.Rp / kOzBM, tn = (N + kOzBN - 1) / kOzBN, nkb = oz.Kp / kOzBK;
+    int splits = std::max(1, std::min(sms / std::max(tm * tn, 1), nkb / 2));
+    while (splits > 1 && (size_t)splits * oz.R * N > ws_doubles) --splits;
+    const int per = (nkb + splits - 1) / splits;
+    return (nkb + per - 1) / per;
+}
+
+void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const OzakiGram& oz,
+                           const int* colmask, double* X, int ldx, double* H, int* status, double* out_sig,
+                           double* out_vr, int kv, int* out_clamped, double* ws, const int* phase_ncol,
+                           const int* phase_splits, unsigned* bar, int max_k, int grid) {
+    const size_t smem = std::max((size_t)OzCfg<kOzSlices>::SMEM,
+                                 sizeof(double) * normalize_smem_doubles<4>(R, true) + 1024 + 16);
+    static size_t attr = 0;
+    if (attr < smem) {
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate_i8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate_i8<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    AERO_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), st));
+    // dev instrumentation (AERO_I8_PROF): CTA-0 ns per segment, printed every 256 launches
+    static unsigned long long* prof = nullptr;
+    static unsigned long long phases = 0, calls = 0;
+    static const bool want = getenv("AERO_I8_PROF") != nullptr;
+    if (want && !prof) {
+        AERO_CUDA(cudaMalloc(&prof, 8 * sizeof(unsigned long long)));
+        AERO_CUDA(cudaMemset(prof, 0, 8 * sizeof(unsigned long long)));
+    }
+    if (prof && ++calls % 256 == 0) {
+        unsigned long long h[8];
+        AERO_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "k_iterate_i8 CTA0 us/phase: tiles %.2f bar1 %.2f normalize %.2f slice %.2f bar2 %.2f (%llu phases)\n",
+                h[0] / 1e3 / phases, h[1] / 1e3 / phases, h[4] / 1e3 / phases, h[2] / 1e3 / phases,
+                h[3] / 1e3 / phases, phases);
+    }
+    phases += (unsigned long long)maxphase;
+    IterI8Args a{jobs, njobs, maxphase, R, ldx, kv, oz.Kp, oz.Rp, X, H, out_sig, out_vr, ws, status, out_clamped,
+                 colmask, phase_ncol, phase_splits, bar, oz.a, oz.ea, oz.b, oz.fb, prof};
+    void* args[] = {&a};
+    note_launch();
+    AERO_CUDA(cudaLaunchCooperativeKernel(max_k <= 2 ? (void*)k_iterate_i8<2> : (void*)k_iterate_i8<4>, dim3(grid),
+                                          dim3(256), args, smem, st));
 }
 
 size_t iterate_smem_bytes(int R) {

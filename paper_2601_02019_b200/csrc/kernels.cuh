@@ -45,9 +45,9 @@ struct OzakiGram {
     int *ea = nullptr, *fb = nullptr;
     size_t a_bytes = 0, b_bytes = 0, ea_n = 0, fb_n = 0;
     void prepare(cudaStream_t st, int R, const double* G, int ldg);
-    // dbg (dev instrumentation, nullable): 8 globaltimer stamps per CTA
     void product(cudaStream_t st, int N, const double* X, int ldx, const int* colmask, double* Y, int ldy,
-                 double* ws, size_t ws_doubles, unsigned long long* dbg = nullptr);
+                 double* ws, size_t ws_doubles);
+    void reserve_x(int N);  // X slice buffers for N columns
     void release();
     ~OzakiGram() { release(); }
 };
@@ -97,6 +97,17 @@ void iter_normalize_ws(cudaStream_t st, const IterJob* jobs, int njobs, int phas
 // the co-resident maximum) is sized to the work so small problems leave the
 // rest of the GPU to concurrent streams (MlState levels)
 int iterate_grid(int R);
+// all phases of a batch in one persistent cooperative launch with the products
+// on the int8 tensor cores (ozaki.cuh tiles; G sliced by oz.prepare, X sliced
+// in the kernel: phase 0 up front, later phases by the normalization as it
+// writes each new iterate); phase_splits[p] split-K ways per phase (partials
+// in ws, summed by the per-job normalization); grid <= number of SMs
+void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const OzakiGram& oz,
+                           const int* colmask, double* X, int ldx, double* H, int* status, double* out_sig,
+                           double* out_vr, int kv, int* out_clamped, double* ws, const int* phase_ncol,
+                           const int* phase_splits, unsigned* bar, int max_k, int grid);
+// split-K ways of an int8 tensor-core product of R rows x N columns (K = R)
+int ozaki_splits(const OzakiGram& oz, int N, size_t ws_doubles);
 void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int maxphase, int R, const double* G,
                         int ldg, double* X, int ldx, double* H, int* status, double* out_sig, double* out_vr,
                         int kv, int* out_clamped, double* ws, const int* phase_ncol, const int* phase_splits,

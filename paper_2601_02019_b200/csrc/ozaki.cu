@@ -45,91 +45,6 @@ constexpr int OZ_BN = kOzBN;  // job columns per CTA (UMMA N)
 constexpr int OZ_BK = kOzBK;  // K bytes (int8 elements) per stage
 constexpr int OZ_THREADS = 256;
 
-template <int S>
-struct OzCfg {
-    static constexpr int A_BYTES = S * OZ_BM * OZ_BK;
-    static constexpr int B_BYTES = S * OZ_BN * OZ_BK;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int SMEM = 2 * STAGE + 1024 + 128 + OZ_BN * 12;  // + alignment slack, barriers, column scales
-    static constexpr int TMEM_COLS = (S * OZ_BN <= 256) ? 256 : 512;
-};
-
-// UMMA instruction descriptor: D s32, A/B signed int8, both K-major, M=128, N=64
-constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
-                              ((uint32_t)(OZ_BM >> 4) << 24);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-// shared-memory matrix descriptor, K-major with the 64-byte swizzle: a tile
-// is rows x 64 B (row m at 64 m, its 16-byte chunk c stored at chunk
-// c ^ ((m >> 1) & 3)); 8-row atoms of 512 B (SBO), LBO unused; the K step of
-// 32 bytes inside the atom advances the start address (the hardware applies
-// the XOR on address bits [4:5] ^= [7:8], so tiles are 1024-byte aligned);
-// descriptor version 1 (sm_100), layout type 4 = SWIZZLE_64B.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(512u >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)4 << 61;
-    return d;
-}
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(kIdescI8), "r"(acc));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n\t"
-        "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-// bulk global -> shared copy completing on an mbarrier (bytes multiple of 16)
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-        "%13, %14, %15}, [%16];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-          "=r"(v[15])
-        : "r"(taddr));
-}
-
 // Slices of `nvec` fp64 vectors of length K (vector i at V + i*ldv; entries
 // at k >= lim_i are zero, lim_i = min(mask[i], K) or K) into the tiled image
 // (ozaki.cuh); vectors nvec.. of the last tile are zero. One CTA per vector.
@@ -150,142 +65,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_product_i8(int M, int N, int Kp, int kb_per_split, const int8_t* __restrict__ As,
                  const int8_t* __restrict__ Bs, const int* __restrict__ ea, const int* __restrict__ fb,
                  double* __restrict__ out, int ldo, int64_t sstride, const int* __restrict__ colmask,
-                 int direct, unsigned long long* __restrict__ dbg) {
+                 int direct) {
     using Cfg = OzCfg<S>;
-    unsigned long long t_0 = 0;
-    if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_0));
-#define OZ_MARK(slot_)                                                                         \
-    if (dbg && threadIdx.x == 0) {                                                              \
-        unsigned long long t_;                                                                  \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
-        const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);        \
-        dbg[cta_ * 8 + (slot_)] = t_;                                                           \
-    }
     extern __shared__ __align__(1024) uint8_t smraw[];
-    // swizzled tiles need 1024-byte aligned shared addresses
-    uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * Cfg::STAGE);
-    uint64_t* empty = full + 2;
-    uint64_t* done = empty + 2;  // one commit after the last stage: accumulators final
-    uint32_t* slot = reinterpret_cast<uint32_t*>(done + 1);
-    double* cscale = reinterpret_cast<double*>(slot + 2);  // OZ_BN per-column 2^(f - 14)
-    int* clim = reinterpret_cast<int*>(cscale + OZ_BN);    // OZ_BN per-column row limits
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int bm = blockIdx.y * OZ_BM, bn = blockIdx.x * OZ_BN, z = blockIdx.z;
-    const int nkb_all = Kp / OZ_BK;
-    const int kb0 = z * kb_per_split;
+    uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);  // swizzled tiles: 1024-B aligned
+    __shared__ uint32_t slot;
+    const int z = blockIdx.z, nkb_all = Kp / OZ_BK, kb0 = z * kb_per_split;
     const int nkb = max(0, min(nkb_all - kb0, kb_per_split));
-
-    if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], 1);
-        }
-        mbar_init(done, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    if (tid < OZ_BN) {
-        const int n = bn + tid;
-        cscale[tid] = (n < N) ? ldexp(1.0, fb[n] - 14) : 0.0;
-        clim[tid] = (n >= N) ? 0 : ((direct && colmask) ? colmask[n] : M);
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)),
+    if ((threadIdx.x >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&slot)),
                      "r"(Cfg::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tmem = *slot;
-    const uint32_t sbase = smem_u32(sm);
-    if (dbg && tid == 0) dbg[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 8] = t_0;
-    OZ_MARK(1);
-
-    if (tid == 0 && nkb > 0) {  // producer + MMA issuer
-        const int8_t* Ablk = As + ((int64_t)blockIdx.y * nkb_all + kb0) * Cfg::A_BYTES;
-        const int8_t* Bblk = Bs + ((int64_t)blockIdx.x * nkb_all + kb0) * Cfg::B_BYTES;
-        auto load = [&](int st, int kb) {
-            const uint32_t dA = sbase + st * Cfg::STAGE;
-            mbar_expect_tx(&full[st], Cfg::STAGE);
-            bulk_g2s(dA, Ablk + (int64_t)kb * Cfg::A_BYTES, Cfg::A_BYTES, &full[st]);
-            bulk_g2s(dA + Cfg::A_BYTES, Bblk + (int64_t)kb * Cfg::B_BYTES, Cfg::B_BYTES, &full[st]);
-        };
-        load(0, 0);
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb & 1;
-            mbar_wait(&full[st], (kb >> 1) & 1);
-            if (kb == 0) OZ_MARK(2);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t aS = sbase + st * Cfg::STAGE, bS = aS + Cfg::A_BYTES;
-#pragma unroll
-            for (int ks = 0; ks < OZ_BK / 32; ++ks) {
-#pragma unroll
-                for (int p = 0; p < S; ++p) {
-                    const uint64_t da = umma_desc(aS + p * OZ_BM * OZ_BK + ks * 32);
-#pragma unroll
-                    for (int q = 0; q < S - p; ++q) {
-                        const uint64_t db = umma_desc(bS + q * OZ_BN * OZ_BK + ks * 32);
-                        mma_i8(tmem + (uint32_t)((p + q) * OZ_BN), da, db, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
-                    }
-                }
-            }
-            umma_commit(&empty[st]);
-            // refill the other stage once the MMAs of kb-1 have drained it
-            // (those of kb are queued behind them, so the tensor pipe stays busy)
-            if (kb + 1 < nkb) {
-                if (kb >= 1) mbar_wait(&empty[st ^ 1], ((kb - 1) >> 1) & 1);
-                load(st ^ 1, kb + 1);
-            }
-        }
-        umma_commit(done);
-        OZ_MARK(3);
-    }
-    __syncwarp();
-
-    // epilogue: warp w reads TMEM lanes 32 (w % 4) + lane = tile row, columns 32 (w / 4) ..
-    const int qd = warp & 3, half = warp >> 2;
-    const int m = bm + qd * 32 + lane;
-    double* o = out + (direct ? 0 : (int64_t)z * sstride);
-    if (nkb > 0) {
-        // (a parity wait on a stage barrier could pass on its not-yet-started
-        // phase; the single-use barrier cannot)
-        mbar_wait(done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    }
-    OZ_MARK(4);
-    const double rs = (m < M) ? ldexp(1.0, ea[m]) : 0.0;
-#pragma unroll 1
-    for (int c16 = 0; c16 < 2; ++c16) {
-        const int c0 = half * 32 + c16 * 16;
-        double acc[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-        if (nkb > 0) {
-            uint32_t v[S][16];
-#pragma unroll
-            for (int t = 0; t < S; ++t)
-                tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(t * OZ_BN + c0), v[t]);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-            for (int t = S - 1; t >= 0; --t)  // Horner in 2^-7: sum_t 2^{-7t} D_t
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] = fma(acc[j], 0x1.0p-7, (double)(int)v[t][j]);
-        }
-        if (m < M) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int c = c0 + j;
-                if (clim[c] == 0) break;
-                o[m + (int64_t)(bn + c) * ldo] = (m < clim[c]) ? (acc[j] * rs) * cscale[c] : 0.0;
-            }
-        }
-    }
-    OZ_MARK(5);
+    const uint32_t tmem = slot;
+    ozaki_tile<S>(M, N, nkb_all, blockIdx.y, blockIdx.x, kb0, nkb, As, Bs, ea, fb,
+                  out + (direct ? 0 : (int64_t)z * sstride), ldo, colmask, direct, sm, tmem);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    OZ_MARK(6);
-    if (warp == 0) {
+    if ((threadIdx.x >> 5) == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
     }
@@ -326,10 +126,7 @@ void OzakiGram::prepare(cudaStream_t st, int R_, const double* G, int ldg) {
     AERO_LAUNCHED();
 }
 
-void OzakiGram::product(cudaStream_t st, int N, const double* X, int ldx, const int* colmask, double* Y,
-                        int ldy, double* ws, size_t ws_doubles, unsigned long long* dbg) {
-    using Cfg = OzCfg<kSlices>;
-    if (N <= 0) return;
+void OzakiGram::reserve_x(int N) {
     const int Np = (N + OZ_BN - 1) / OZ_BN * OZ_BN;
     const size_t need = (size_t)kSlices * Np * Kp;
     if (b_bytes < need) {
@@ -342,6 +139,14 @@ void OzakiGram::product(cudaStream_t st, int N, const double* X, int ldx, const 
         AERO_CUDA(cudaMalloc(&fb, sizeof(int) * Np));
         fb_n = Np;
     }
+}
+
+void OzakiGram::product(cudaStream_t st, int N, const double* X, int ldx, const int* colmask, double* Y,
+                        int ldy, double* ws, size_t ws_doubles) {
+    using Cfg = OzCfg<kSlices>;
+    if (N <= 0) return;
+    const int Np = (N + OZ_BN - 1) / OZ_BN * OZ_BN;
+    reserve_x(N);
     k_ozaki_slice<kSlices, OZ_BN><<<Np, SL_THREADS, 0, st>>>(N, R, Kp, X, ldx, colmask, b, fb);
     AERO_LAUNCHED();
     static bool attr = false;
@@ -362,7 +167,7 @@ void OzakiGram::product(cudaStream_t st, int N, const double* X, int ldx, const 
     const int ldo = direct ? ldy : R;
     const int64_t sstride = (int64_t)R * N;
     k_product_i8<kSlices><<<dim3(tn, tm, splits), OZ_THREADS, Cfg::SMEM, st>>>(
-        R, N, Kp, per, a, b, ea, fb, o, ldo, sstride, colmask, direct, dbg);
+        R, N, Kp, per, a, b, ea, fb, o, ldo, sstride, colmask, direct);
     AERO_LAUNCHED();
     if (!direct) {
         const int64_t tot = (int64_t)R * N;

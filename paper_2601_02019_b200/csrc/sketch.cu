@@ -282,6 +282,38 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
             prof.product_flops += flops;
         }
         maxphase = 1;
+    } else if (i8_ && R >= i8_min_rows_ && persistent_ && max_k <= 4 && maxphase <= kMaxPhases) {
+        // large buffers: all phases in one cooperative launch, products on the
+        // int8 tensor cores (kernels.cu k_iterate_i8)
+        oz_.prepare(st_, R, G_.p, cap_);
+        double flops = 0.0;
+        for (int p = 0; p < maxphase; ++p) {
+            int ncol = 0;
+            for (int j = 0; j < njobs; ++j)
+                if (jobs_h_[j].nphase > p) {
+                    ncol = std::max(ncol, jobs_h_[j].col + jobs_h_[j].k);
+                    flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
+                }
+            ncol = std::max(ncol, 1);
+            phase_h_[p] = ncol;
+            phase_h_[kMaxPhases + p] = ozaki_splits(oz_, ncol, ws_.n);
+        }
+        oz_.reserve_x(phase_h_[0]);
+        AERO_CUDA(cudaMemcpyAsync(phase_d_, phase_h_, sizeof(int) * 2 * kMaxPhases, cudaMemcpyHostToDevice, st_));
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
+        static int sms = 0;
+        if (!sms) AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_));
+        iterate_i8_persistent(st_, jobs_d_, njobs, maxphase, R, oz_, colmask_d_, X_.p, ldx_, H_.p, status_d_,
+                              sig_.p, vr_.p, kv_, clamp_d_, ws_.p, phase_d_, phase_d_ + kMaxPhases, bar_d_, max_k,
+                              sms);
+        if (profiling) {
+            AERO_CUDA(cudaEventRecord(ev_at(3), st_));
+            prof.product_launches++;
+            prof.product_flops += flops;
+        }
+        maxphase = 1;  // one timed region below
     } else if (max_k <= 4 && maxphase <= kMaxPhases && persistent_ && small_phases) {
         // all phases in one cooperative launch (kernels.cu k_iterate)
         const int kt = (R + 15) / 16;

@@ -258,13 +258,16 @@ def test_persistent_iterate_matches_launch_sequence(orc, monkeypatch):
     assert_trace_equal(ev_a, ref.update_block(rows, ts))
 
 
+@pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("cfg", ["c1", "ell128", "ell512"])
-def test_int8_tensor_product_iterate_parity(orc, monkeypatch, cfg):
+def test_int8_tensor_product_iterate_parity(orc, monkeypatch, cfg, persistent):
     """The iteration products on the int8 tensor cores (ozaki.cu), forced on
-    for every buffer size (AERO_I8_MIN_ROWS=1; per-phase launch sequence),
-    keep the decision trace identical to the oracle's and the sketch within
-    the fp64 tolerances."""
-    monkeypatch.setenv("AERO_NO_PERSISTENT", "1")
+    for every buffer size above the warp kernel's (AERO_I8_MIN_ROWS=1), as the
+    per-phase launch sequence and as the persistent cooperative kernel
+    (kernels.cu k_iterate_i8), keep the decision trace identical to the
+    oracle's and the sketch within the fp64 tolerances."""
+    if not persistent:
+        monkeypatch.setenv("AERO_NO_PERSISTENT", "1")
     monkeypatch.setenv("AERO_I8_MIN_ROWS", "1")
     if cfg == "c1":
         d, eps, seed, n = 1024, 1 / 16, 1, 900
