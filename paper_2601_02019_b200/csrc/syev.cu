@@ -42,6 +42,7 @@ constexpr int TRD_THREADS = 256;  // 8 warps
 constexpr int TRD_TILE = 64;      // trailing-update tile
 constexpr int SLOTW = 4;          // doubles per CTA partial slot
 constexpr int BT_NB = 128;        // reflectors per back-transform block
+constexpr int TRD_DSPLIT = 4;     // warps per panel dot product
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -181,35 +182,28 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
                 for (int r = j + 1 + gw; r < n; r += GW) {
                     const double* col = A + (int64_t)r * lda + c0;
                     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-                    if (VEC) {  // 8 x 16 B loads in flight per lane
+                    if (VEC) {  // 16 x 16 B loads in flight per lane (two L2 round trips per n=2048 column)
                         const double2* c2 = reinterpret_cast<const double2*>(col);
                         const double2* v2 = reinterpret_cast<const double2*>(sv);
                         const int np = len >> 1;
-                        int p = lane;
-                        for (; p + 224 < np; p += 256) {
-                            double2 x[8];
+                        for (int p0 = 0; p0 < np; p0 += 32 * 16) {
+                            double2 x[16];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) x[u] = __ldcg(c2 + p + 32 * u);
+                            for (int u = 0; u < 16; ++u) {
+                                const int idx = p0 + lane + 32 * u;
+                                x[u] = (idx < np) ? __ldcg(c2 + idx) : make_double2(0.0, 0.0);
+                            }
 #pragma unroll
-                            for (int u = 0; u < 8; u += 4) {
-                                const double2 y0 = v2[p + 32 * u], y1 = v2[p + 32 * (u + 1)];
-                                const double2 y2 = v2[p + 32 * (u + 2)], y3 = v2[p + 32 * (u + 3)];
-                                acc0 = fma(x[u].x, y0.x, fma(x[u].y, y0.y, acc0));
-                                acc1 = fma(x[u + 1].x, y1.x, fma(x[u + 1].y, y1.y, acc1));
-                                acc2 = fma(x[u + 2].x, y2.x, fma(x[u + 2].y, y2.y, acc2));
-                                acc3 = fma(x[u + 3].x, y3.x, fma(x[u + 3].y, y3.y, acc3));
+                            for (int u = 0; u < 16; u += 4) {
+#pragma unroll
+                                for (int w = 0; w < 4; ++w) {
+                                    const int idx = p0 + lane + 32 * (u + w);
+                                    const double2 y = (idx < np) ? v2[idx] : make_double2(0.0, 0.0);
+                                    double& acc = (w == 0) ? acc0 : (w == 1) ? acc1 : (w == 2) ? acc2 : acc3;
+                                    acc = fma(x[u + w].x, y.x, fma(x[u + w].y, y.y, acc));
+                                }
                             }
                         }
-                        double2 x[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            x[u] = (p + 32 * u < np) ? __ldcg(c2 + p + 32 * u) : make_double2(0.0, 0.0);
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (p + 32 * u < np) {
-                                const double2 y = v2[p + 32 * u];
-                                acc0 = fma(x[u].x, y.x, fma(x[u].y, y.y, acc0));
-                            }
                         if ((len & 1) && lane == 0) acc1 = fma(col[len - 1], sv[len - 1], acc1);
                     } else {
                         int c = lane;
@@ -224,26 +218,31 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
                     const double acc = warp_sum_d((acc0 + acc1) + (acc2 + acc3));
                     if (lane == 0) a.ybuf[r] = acc;
                 }
-                for (int q = GW - 1 - gw; q < 2 * jj; q += GW) {
+                // panel dots, each split over TRD_DSPLIT warps (contiguous row
+                // quarters; the consumer sums the parts in fixed order)
+                for (int qq = GW - 1 - gw; qq < 2 * jj * TRD_DSPLIT; qq += GW) {
+                    const int q = qq / TRD_DSPLIT, part = qq % TRD_DSPLIT;
+                    const int span = (n - j - 1 + TRD_DSPLIT - 1) / TRD_DSPLIT;
+                    const int cs = j + 1 + part * span, ce = min(n, cs + span);
                     double acc0 = 0.0, acc1 = 0.0;
                     if (q < jj) {  // V(:, i0+q)^T v
                         const double* col = V + (int64_t)(i0 + q) * n;
-                        for (int c = j + 1 + lane; c < n; c += 64) {
+                        for (int c = cs + lane; c < ce; c += 64) {
                             acc0 = fma(__ldcg(col + c), sv[c - c0], acc0);
-                            if (c + 32 < n) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
+                            if (c + 32 < ce) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
                         }
                     } else if (q - jj < jj - 1) {  // W(:, k)^T v, final columns
                         const double* col = W + (int64_t)(q - jj) * n;
-                        for (int c = j + 1 + lane; c < n; c += 64) {
+                        for (int c = cs + lane; c < ce; c += 64) {
                             acc0 = fma(__ldcg(col + c), sv[c - c0], acc0);
-                            if (c + 32 < n) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
+                            if (c + 32 < ce) acc1 = fma(__ldcg(col + c + 32), sv[c + 32 - c0], acc1);
                         }
                     } else {  // W(:, jj-1) = wpre + alpha2 v_prev
-                        for (int c = j + 1 + lane; c < n; c += 32)
+                        for (int c = cs + lane; c < ce; c += 32)
                             acc0 = fma(__ldcg(a.wpre + c) + a2prev * svo[c - c0prev], sv[c - c0], acc0);
                     }
                     const double acc = warp_sum_d(acc0 + acc1);
-                    if (lane == 0) a.dots[q] = acc;
+                    if (lane == 0) a.dots[qq] = acc;
                 }
             }
             // own-row panel values (final before this column) and the panel part of y0
@@ -277,7 +276,13 @@ __global__ void __launch_bounds__(TRD_THREADS, 1) k_sytrd(TrdArgs a) {
             TRD_MARK(2);
 
             // ---- C: own rows
-            if (tid < 2 * jj) sdot[tid] = (tau != 0.0) ? __ldcg(a.dots + tid) : 0.0;
+            if (tid < 2 * jj) {
+                double v = 0.0;
+                if (tau != 0.0)
+#pragma unroll
+                    for (int pt = 0; pt < TRD_DSPLIT; ++pt) v += __ldcg(a.dots + tid * TRD_DSPLIT + pt);
+                sdot[tid] = v;
+            }
             const double yb = (valid && sub == 0 && tau != 0.0) ? __ldcg(a.ybuf + r) : 0.0;
             __syncthreads();
             double t = 0.0;
@@ -1164,7 +1169,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     const size_t n2 = (size_t)n * n;
     wk.V.alloc(n2);
     wk.W.alloc((size_t)n * TRD_NB);
-    wk.vec.alloc((size_t)11 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB + 8);
+    wk.vec.alloc((size_t)11 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB * TRD_DSPLIT + 8);
     double* d = wk.vec.p;
     double* e = d + n;
     double* tau = e + n;
@@ -1175,7 +1180,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     double* lam = e2 + n;
     double* slots = lam + n + n;
     double* dots = slots + SLOTW * wk.grid;
-    double* bounds = dots + 2 * TRD_NB;
+    double* bounds = dots + 2 * TRD_NB * TRD_DSPLIT;
     int* blk = reinterpret_cast<int*>(bounds + 8);       // 2n ints
     int* order = blk + 2 * n;                            // n ints
     fill_zero(st, wk.V.p, (int64_t)n2);
