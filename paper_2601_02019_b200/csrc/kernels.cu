@@ -490,7 +490,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                               int* __restrict__ status, double* __restrict__ out_sig,
                               double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
                               const double* __restrict__ ws, int wsM, int64_t sstride, int splits,
-                              double* sm) {
+                              double* sm, const OzSliceDst xs = OzSliceDst{}) {
     if (phase >= jb.nphase) return;
     const int st = status[jidx];
     const bool last = (phase == jb.nphase - 1);
@@ -553,15 +553,36 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     }
     if (jb.type == 0) {
         if (!last) {
-            double s = 0.0;
-            for (int i = tid; i < r; i += nt) s = fma(y[i], y[i], s);
+            double s = 0.0, mx = 0.0;
+            for (int i = tid; i < r; i += nt) {
+                const double v = y[i];
+                s = fma(v, v, s);
+                mx = fmax(mx, fabs(v));
+            }
+            if (xs.b) {  // max |y| for the slicing scale (max |x| = fl(max|y| / nrm))
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if ((tid & 31) == 0) red[64 + (tid >> 5)] = mx;
+            }
             s = block_sum(s, red);
             const double nrm = sqrt(s);
             if (nrm < 1e-300) {  // linalg.cpp:112-116
                 if (tid == 0) status[jidx] = JOB_DEAD;
                 return;
             }
-            for (int i = tid; i < r; i += nt) x[i] = y[i] / nrm;
+            int e = 0;
+            if (xs.b) {
+                mx = 0.0;
+                for (int w = 0; w < (nt + 31) / 32; ++w) mx = fmax(mx, red[64 + w]);
+                const double xm = mx / nrm;
+                e = (xm > 0.0) ? ilogb(xm) + 1 : 0;
+                if (tid == 0) xs.fe[jb.col] = e;
+            }
+            for (int i = tid; i < r; i += nt) {
+                const double v = y[i] / nrm;
+                x[i] = v;
+                if (xs.b) ozaki_store_value<kOzSlices, kOzBN>(xs.b, xs.Kp, jb.col, i, v, e);
+            }
         } else {
             double s = 0.0;  // sigma1^2 = ||A x||^2 = x^T G x (linalg.cpp:119)
             for (int i = tid; i < r; i += nt) s = fma(x[i], y[i], s);
@@ -595,9 +616,15 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
     __syncthreads();
     // rows independent: [last: H = X T], X <- Y T; RU rows per thread per
-    // round with all their loads issued first (one L2 round trip per round)
+    // round with all their loads issued first (one L2 round trip per round).
+    // With xs (not last): the new columns are also sliced for the next product
+    // -- from registers when the job fits one round, else reloaded below.
     {
         constexpr int RU = (KM <= 4) ? 16 / KM : 1;
+        const bool slice_regs = xs.b && !last && r <= RU * nt;
+        double hv[RU][KM], mxb[KM];
+#pragma unroll
+        for (int b = 0; b < KM; ++b) mxb[b] = 0.0;
         for (int i0 = tid; i0 < r; i0 += RU * nt) {
             double xr[RU][KM], yr[RU][KM];
 #pragma unroll
@@ -628,8 +655,37 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                     }
                     if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;
                     x[i + (int64_t)b * ldx] = hy;
+                    hv[u][b] = hy;
+                    mxb[b] = fmax(mxb[b], fabs(hy));
                 }
             }
+        }
+        if (slice_regs) {
+#pragma unroll
+            for (int b = 0; b < KM; ++b) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mxb[b] = fmax(mxb[b], __shfl_xor_sync(0xffffffffu, mxb[b], o));
+                if ((tid & 31) == 0) red[64 + b * 32 + (tid >> 5)] = mxb[b];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < KM; ++b) {
+                if (b >= k) break;
+                double m = 0.0;
+                for (int w = 0; w < (nt + 31) / 32; ++w) m = fmax(m, red[64 + b * 32 + w]);
+                const int e = (m > 0.0) ? ilogb(m) + 1 : 0;
+                if (tid == 0) xs.fe[jb.col + b] = e;
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const int i = tid + u * nt;
+                    if (i < r) ozaki_store_value<kOzSlices, kOzBN>(xs.b, xs.Kp, jb.col + b, i, hv[u][b], e);
+                }
+            }
+        } else if (xs.b && !last) {
+            __syncthreads();
+            for (int b = 0; b < k; ++b)
+                ozaki_slice_vector<kOzSlices, kOzBN>(x + (int64_t)b * ldx, r, xs.Kp, jb.col + b, xs.b, xs.fe,
+                                                     red + 64);
         }
     }
     __syncthreads();
@@ -802,19 +858,11 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
         for (int j = blockIdx.x; j < a.njobs; j += G) {
             const IterJob jb = a.jobs[j];
             __syncthreads();
+            // the normalization also slices the new iterate for the next product
             normalize_job<KM, true>(jb, j, p, a.X, nullptr, a.ldx, a.H, a.status, a.out_sig, a.out_vr, a.kv,
-                                    a.out_clamped, a.ws, R, sstride, splits, smd);
+                                    a.out_clamped, a.ws, R, sstride, splits, smd, OzSliceDst{a.xb, a.xfe, a.Kp});
             __syncthreads();
             if (j == 0) I8_MARK(4);
-            if (p + 1 < jb.nphase && *(volatile int*)(a.status + j) == JOB_ACTIVE) {
-                if (jb.k == 2)  // both columns in one pass (one shared reduction)
-                    ozaki_slice_vectors<S, kOzBN, 2>(a.X + (int64_t)jb.col * a.ldx, a.ldx, jb.r, a.Kp, jb.col, a.xb,
-                                                     a.xfe, smd);
-                else
-                    for (int c = 0; c < jb.k; ++c)
-                        ozaki_slice_vector<S, kOzBN>(a.X + (int64_t)(jb.col + c) * a.ldx, jb.r, a.Kp, jb.col + c,
-                                                     a.xb, a.xfe, smd);
-            }
         }
         I8_MARK(2);
         grid_sync(a.bar, epoch, G);

@@ -94,6 +94,29 @@ __device__ inline void ozaki_slice_vectors(const double* __restrict__ v0, int ld
     }
 }
 
+// Destination of slices written as a side effect of the normalization (the
+// X image of the next product); b == nullptr: none
+struct OzSliceDst {
+    int8_t* b = nullptr;
+    int* fe = nullptr;
+    int Kp = 0;
+};
+
+// the S slices of one value x (|x| < 2^e) at K index k of vector i, as bytes
+// of the tiled image (TR vectors per tile)
+template <int S, int TR>
+__device__ __forceinline__ void ozaki_store_value(int8_t* __restrict__ out, int Kp, int i, int k, double x, int e) {
+    const int nkb = Kp / kOzBK, t = i / TR, r = i % TR, b = k / kOzBK, kk = k % kOzBK, kc = kk >> 4;
+    int8_t* base = out + ((int64_t)t * nkb + b) * S * TR * kOzBK + r * kOzBK + ((kc ^ ((r >> 1) & 3)) << 4) + (kk & 15);
+    double y = scalbn(x, 7 - e);  // |y| < 128
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+        const double sv = trunc(y);
+        y = (y - sv) * 128.0;
+        base[p * TR * kOzBK] = (int8_t)(int)sv;
+    }
+}
+
 // Slice vector i (v[0..lim), zero beyond; padded to Kp) into the product
 // kernel's tiled image: tiles of TR vectors; block (tile t, K block b) at
 // out + (t * nkb + b) * S * TR * 64 holds slice p at p * TR * 64, vector row r
