@@ -484,6 +484,16 @@ __host__ __device__ constexpr size_t normalize_smem_doubles(int R, bool ws) {
 
 // one job's normalization after product phase `phase` (body of k_iter_normalize;
 // also run inside the persistent k_iterate); sm: normalize_smem_doubles
+// dev instrumentation (AERO_I8_PROF): CTA-0 ns per normalization step
+__device__ unsigned long long* g_norm_prof = nullptr;
+#define NJ_MARK(i)                                                                 \
+    if (g_norm_prof && blockIdx.x == 0 && threadIdx.x == 0) {                      \
+        unsigned long long t_;                                                     \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+        g_norm_prof[i] += t_ - nj_t;                                               \
+        nj_t = t_;                                                                 \
+    }
+
 template <int KM, bool WS>
 __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                               const double* __restrict__ Y, int ldx, double* H,
@@ -504,6 +514,8 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     double* lam = T + KM * KM;         // KM
     double* cs = lam + KM;             // jacobi scratch
     double* ysh = cs + jacobi_scratch_doubles(KM);  // WS: r * k
+    unsigned long long nj_t = 0;
+    if (g_norm_prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nj_t));
     if (st != JOB_ACTIVE) {
         if (last && tid == 0) {
             if (jb.type == 0) out_sig[jb.col] = 0.0;
@@ -545,6 +557,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 if (ok[u]) ysh[e0 + u * nt] = v[u];
         }
         __syncthreads();
+        NJ_MARK(0);
         y = ysh;
         ldy = r;
     } else {
@@ -593,6 +606,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     }
     // simul: S = X^T Y (Gram of g = C'^T X), T = S^{-1/2}
     cta_gram<KM>(x, ldx, y, ldy, r, k, S, red);
+    NJ_MARK(1);
     for (int e = tid; e < k * k; e += nt) {
         const int a = e % k, b = e / k;
         W[e] = 0.5 * (S[a + b * k] + S[b + a * k]);
@@ -615,6 +629,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     __syncthreads();
     for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
     __syncthreads();
+    NJ_MARK(2);
     // rows independent: [last: H = X T], X <- Y T; RU rows per thread per
     // round with all their loads issued first (one L2 round trip per round).
     // With xs (not last): the new columns are also sliced for the next product
@@ -660,6 +675,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 }
             }
         }
+        NJ_MARK(3);
         if (slice_regs) {
 #pragma unroll
             for (int b = 0; b < KM; ++b) {
@@ -687,6 +703,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 ozaki_slice_vector<kOzSlices, kOzBN>(x + (int64_t)b * ldx, r, xs.Kp, jb.col + b, xs.b, xs.fe,
                                                      red + 64);
         }
+        NJ_MARK(4);
     }
     __syncthreads();
     if (!last) return;
@@ -896,6 +913,7 @@ void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int 
                            const int* colmask, double* X, int ldx, double* H, int* status, double* out_sig,
                            double* out_vr, int kv, int* out_clamped, double* ws, const int* phase_ncol,
                            const int* phase_splits, unsigned* bar, int max_k, int grid) {
+    // the tile pipeline's stages or the normalization's scratch (phases are separate in time)
     const size_t smem = std::max((size_t)OzCfg<kOzSlices>::SMEM,
                                  sizeof(double) * normalize_smem_doubles<4>(R, true) + 1024 + 16);
     static size_t attr = 0;
@@ -909,9 +927,13 @@ void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int 
     static unsigned long long* prof = nullptr;
     static unsigned long long phases = 0, calls = 0;
     static const bool want = getenv("AERO_I8_PROF") != nullptr;
+    static unsigned long long* nprof = nullptr;
     if (want && !prof) {
         AERO_CUDA(cudaMalloc(&prof, 8 * sizeof(unsigned long long)));
         AERO_CUDA(cudaMemset(prof, 0, 8 * sizeof(unsigned long long)));
+        AERO_CUDA(cudaMalloc(&nprof, 8 * sizeof(unsigned long long)));
+        AERO_CUDA(cudaMemset(nprof, 0, 8 * sizeof(unsigned long long)));
+        AERO_CUDA(cudaMemcpyToSymbol(g_norm_prof, &nprof, sizeof(nprof)));
     }
     if (prof && ++calls % 256 == 0) {
         unsigned long long h[8];
@@ -919,6 +941,10 @@ void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int 
         fprintf(stderr, "k_iterate_i8 CTA0 us/phase: tiles %.2f bar1 %.2f normalize %.2f slice %.2f bar2 %.2f (%llu phases)\n",
                 h[0] / 1e3 / phases, h[1] / 1e3 / phases, h[4] / 1e3 / phases, h[2] / 1e3 / phases,
                 h[3] / 1e3 / phases, phases);
+        AERO_CUDA(cudaMemcpy(h, nprof, sizeof(h), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "  normalize CTA0 us/phase: ws-sum %.2f gram %.2f eig %.2f update %.2f slice %.2f\n",
+                h[0] / 1e3 / phases, h[1] / 1e3 / phases, h[2] / 1e3 / phases, h[3] / 1e3 / phases,
+                h[4] / 1e3 / phases);
     }
     phases += (unsigned long long)maxphase;
     IterI8Args a{jobs, njobs, maxphase, R, ldx, kv, oz.Kp, oz.Rp, X, H, out_sig, out_vr, ws, status, out_clamped,

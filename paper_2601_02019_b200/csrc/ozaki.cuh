@@ -108,7 +108,8 @@ template <int S, int TR>
 __device__ __forceinline__ void ozaki_store_value(int8_t* __restrict__ out, int Kp, int i, int k, double x, int e) {
     const int nkb = Kp / kOzBK, t = i / TR, r = i % TR, b = k / kOzBK, kk = k % kOzBK, kc = kk >> 4;
     int8_t* base = out + ((int64_t)t * nkb + b) * S * TR * kOzBK + r * kOzBK + ((kc ^ ((r >> 1) & 3)) << 4) + (kk & 15);
-    double y = scalbn(x, 7 - e);  // |y| < 128
+    // exact power-of-two scaling (|x| < 2^e, e far from the exponent limits)
+    double y = (e > -900 && e < 900) ? x * __longlong_as_double((long long)(1023 + 7 - e) << 52) : scalbn(x, 7 - e);
 #pragma unroll
     for (int p = 0; p < S; ++p) {
         const double sv = trunc(y);
