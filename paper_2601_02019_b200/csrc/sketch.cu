@@ -1,6 +1,8 @@
 // AeroState engine on one B200 (see sketch.hpp). Control flow restates
 // /root/reference/proj/src/sketch.cpp:82-141 row by row; device work is
 // batched speculatively across rows.
+#include <chrono>
+#include <cstdio>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -136,6 +138,9 @@ cudaEvent_t Sketch::ev_at(size_t i) {
 }
 
 Sketch::~Sketch() {
+    if (getenv("AERO_HOST_PROF") && host_syncs_ > 0)
+        fprintf(stderr, "sketch host: process_rows wall %.1f ms, blocked in iterate syncs %.1f ms over %lld syncs (%.1f us/sync)\n",
+                host_wall_s_ * 1e3, host_sync_s_ * 1e3, (long long)host_syncs_, host_sync_s_ * 1e6 / host_syncs_);
     cudaSetDevice(dev_);
     if (st_) cudaStreamSynchronize(st_);
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
@@ -399,7 +404,10 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     AERO_CUDA(cudaMemcpyAsync(sig_h_, sig_.p, sizeof(double) * ncol_total, cudaMemcpyDeviceToHost, st_));
     AERO_CUDA(cudaMemcpyAsync(status_h_, status_d_, sizeof(int) * njobs, cudaMemcpyDeviceToHost, st_));
     AERO_CUDA(cudaMemcpyAsync(clamp_h_, clamp_d_, sizeof(int) * njobs, cudaMemcpyDeviceToHost, st_));
+    const auto hs0 = std::chrono::steady_clock::now();
     AERO_CUDA(cudaStreamSynchronize(st_));
+    host_sync_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - hs0).count();
+    host_syncs_++;
     if (profiling) {
         float ms = 0.f;
         AERO_CUDA(cudaEventElapsedTime(&ms, ev_at(0), ev_at(1)));
@@ -690,6 +698,12 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
 
 void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
                           const double* thetas, aero_event* log) {
+    const auto hw0 = std::chrono::steady_clock::now();
+    struct WallAcc {  // dev instrumentation (AERO_HOST_PROF): wall time of process_rows
+        double& acc;
+        std::chrono::steady_clock::time_point t0;
+        ~WallAcc() { acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+    } wall_acc{host_wall_s_, hw0};
     int64_t pos = 0;
     while (pos < n) {
         const int64_t room = (int64_t)cap_ - 1 - r_;  // rows that fit before a reduce

@@ -141,6 +141,8 @@ class Sketch {
     // n = 128..192 it beats DMMA); AERO_I8_MIN_ROWS overrides (tests force it on)
     int i8_min_rows_ = getenv("AERO_I8_MIN_ROWS") ? atoi(getenv("AERO_I8_MIN_ROWS")) : 1024;
     OzakiGram oz_;
+    double host_wall_s_ = 0.0, host_sync_s_ = 0.0;  // dev instrumentation (AERO_HOST_PROF)
+    int64_t host_syncs_ = 0;
     int* status_d_ = nullptr;
     int* clamp_d_ = nullptr;
     int* colmask_d_ = nullptr;
