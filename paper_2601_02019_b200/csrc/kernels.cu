@@ -516,12 +516,17 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     double* ysh = cs + jacobi_scratch_doubles(KM);  // WS: r * k
     unsigned long long nj_t = 0;
     if (g_norm_prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nj_t));
-    if (st != JOB_ACTIVE) {
+    auto inactive = [&]() {
         if (last && tid == 0) {
             if (jb.type == 0) out_sig[jb.col] = 0.0;
             else
                 for (int a = 0; a < k; ++a) out_sig[jb.col + a] = 0.0;
         }
+    };
+    // WS: the split-K loads are issued before the status is known (the sum
+    // is harmless for an inactive job), so the status round trip overlaps them
+    if (!WS && st != JOB_ACTIVE) {
+        inactive();
         return;
     }
     const double* y;
@@ -558,6 +563,10 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
         }
         __syncthreads();
         NJ_MARK(0);
+        if (st != JOB_ACTIVE) {
+            inactive();
+            return;
+        }
         y = ysh;
         ldy = r;
     } else {
@@ -850,6 +859,8 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
         }
     }
     grid_sync(a.bar, epoch, G);
+    // this CTA's first job, read once (jobs are fixed for the whole launch)
+    const IterJob jb0 = ((int)blockIdx.x < a.njobs) ? a.jobs[blockIdx.x] : IterJob{};
     const bool pr = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
     unsigned long long tp = pr ? gtimer() : 0;
 #define I8_MARK(i)                              \
@@ -873,7 +884,7 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
         grid_sync(a.bar, epoch, G);
         I8_MARK(1);
         for (int j = blockIdx.x; j < a.njobs; j += G) {
-            const IterJob jb = a.jobs[j];
+            const IterJob jb = (j == (int)blockIdx.x) ? jb0 : a.jobs[j];
             __syncthreads();
             // the normalization also slices the new iterate for the next product
             normalize_job<KM, true>(jb, j, p, a.X, nullptr, a.ldx, a.H, a.status, a.out_sig, a.out_vr, a.kv,
