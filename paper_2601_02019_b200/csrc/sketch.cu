@@ -724,7 +724,8 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
         // worth of products) and commits (1-(1-p)^B)/p rows on average, which
         // is cheapest per row near B* = sqrt(2 alpha / (beta p))
         const double p = std::max(end_rate_, 1e-4);
-        cur_batch_ = (int)std::clamp(std::sqrt(52.0 / p), 16.0, (double)max_batch_);
+        static const double two_alpha = getenv("AERO_BATCH_2ALPHA") ? atof(getenv("AERO_BATCH_2ALPHA")) : 52.0;
+        cur_batch_ = (int)std::clamp(std::sqrt(two_alpha / p), 16.0, (double)max_batch_);
         const int64_t B = std::min<int64_t>({(int64_t)cur_batch_, n - pos, room});
         const int64_t mp0 = mispredicts;
         const int64_t used = run_batch(dev_rows + (size_t)pos * d_, B, t + pos, thetas + pos, log + pos);
