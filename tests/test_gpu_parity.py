@@ -555,3 +555,31 @@ def test_int8_tensor_product_matches_fp64(r, n):
         assert np.all(err <= tol + 1e-300), (mode, float(np.max(err / np.maximum(tol, 1e-300))))
         for j in range(n):
             assert np.all(y[mask[j]:, j] == 0.0)
+
+
+def test_c2_scale_default_path_properties(orc):
+    """BASELINE config C2 (d=4096, eps=1/512, ell=1024) at a prefix that
+    crosses the first FD reduce, on the default engine path (speculative
+    batches on the persistent int8 tensor-core iterate once the buffer holds
+    >= 1024 rows, grid-eigensolver reduce at n = 2048): the reduce schedule is
+    data-independent and must be bit-exact (row 2*ell, then every ell+1 rows),
+    the run is deterministic, and the covariance error of the query stays
+    <= eps (the reference's own empirical criterion, test_attp.cpp:81)."""
+    d, eps, n = 4096, 1 / 512, 2600
+    rows = orc.gen_rows(d, 256, 0.99, 0.05, 256.0, 1, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    runs = []
+    for _ in range(2):
+        s = prod.AttpState(d, eps, seed=1, stream=1000)
+        ev = s.update_block(rows, ts)
+        runs.append((ev, s.query(n)))
+    ev, b = runs[0]
+    assert np.array_equal(np.nonzero(ev["reduced"])[0], [2047])
+    assert ev["rows_after"][2047] == 1023 and ev["rows_after"][-1] == 1023 + (n - 2048)
+    assert ev["gate_fired"].mean() > 0.5
+    for f in TRACE_FIELDS:
+        assert np.array_equal(runs[1][0][f], ev[f]), f
+    assert np.array_equal(runs[1][1], b)
+    g = orc.OracleGram(d)
+    g.add_block(rows, ts)
+    assert g.error(b) <= eps
