@@ -1165,7 +1165,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     // CTAs: enough that the symv columns spread, few enough that barriers stay cheap
     // CTAs: enough that the symv columns spread (and 4 rows per warp cover n),
     // few enough that barriers stay cheap
-    const int G = std::max((n + 31) / 32, std::min(wk.grid, (n + 13) / 14));
+    static const int g_env = getenv("AERO_SYTRD_CTAS") ? atoi(getenv("AERO_SYTRD_CTAS")) : 0;  // dev sweep
+    const int G = std::max((n + 31) / 32, std::min(g_env > 0 ? g_env : wk.grid, (n + 13) / 14));
     const size_t n2 = (size_t)n * n;
     wk.V.alloc(n2);
     wk.W.alloc((size_t)n * TRD_NB);
