@@ -657,14 +657,24 @@ __global__ void k_tri_prep(int n, const double* __restrict__ d, double* __restri
         e2[i] = split ? 0.0 : ei * ei;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // block boundaries (sequential scan, n <= 4096)
-        int st = 0;
-        for (int i = 0; i < n; ++i) {
-            blk[i] = st;
-            if (i == n - 1 || e[i] == 0.0) {
-                for (int k = st; k <= i; ++k) blk[n + k] = i + 1;
-                st = i + 1;
-            }
+    if (threadIdx.x < 32) {  // block boundaries: warp scans over 32-row chunks (ballot masks)
+        int carry = 0;         // first row of the block open at the chunk start
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            const bool f = i < n && (i == n - 1 || e[i] == 0.0);  // a block ends at row i
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            const unsigned below = m & ((1u << lane) - 1u);
+            if (i < n) blk[i] = below ? base + (31 - __clz(below)) + 1 : carry;
+            if (m) carry = base + (31 - __clz(m)) + 1;
+        }
+        int carry2 = n;  // one past the end of the block continuing after the chunk
+        for (int base = ((n - 1) / 32) * 32; base >= 0; base -= 32) {
+            const int i = base + lane;
+            const bool f = i < n && (i == n - 1 || e[i] == 0.0);
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            const unsigned here = m & ~((1u << lane) - 1u);
+            if (i < n) blk[n + i] = here ? base + __ffs(here) : carry2;
+            if (m) carry2 = base + __ffs(m);
         }
     }
 }
