@@ -694,24 +694,20 @@ __device__ __forceinline__ int sturm_count(int s, int t, const double* d, const 
     return cnt;
 }
 
-// coarse cut: the largest of 1023 evenly spaced points x with global count(x)
-// <= kc (a lower bound of the kc-th smallest eigenvalue) -> bounds[4]; one
-// Sturm sequence per thread, all in parallel
-__global__ void __launch_bounds__(1024) k_cut_coarse(int n, int kc, const double* __restrict__ d,
-                                                     const double* __restrict__ e2, double* __restrict__ bounds) {
-    __shared__ int best[32];
+// coarse cut: global Sturm counts at 1023 evenly spaced points x_m (one
+// thread each, spread over 32 CTAs so the division chains run on 32 SMs);
+// k_bisect derives from them the largest x_m with count(x_m) <= kc (a lower
+// bound of the kc-th smallest eigenvalue) -- bounds[5] = 1 marks them valid,
+// bounds[6] = kc
+__global__ void __launch_bounds__(32) k_cut_coarse(int n, int kc, const double* __restrict__ d,
+                                                   const double* __restrict__ e2, double* __restrict__ bounds,
+                                                   int* __restrict__ hist) {
     const double lo = bounds[0], hi = bounds[1], pivmin = bounds[2];
-    const int m = threadIdx.x;
-    const double x = lo + (hi - lo) * (double)(m + 1) / 1024.0;
-    const int c = (m < 1023) ? sturm_count(0, n, d, e2, x, pivmin) : n;
-    int cand = (c <= kc) ? m : -1;
-    for (int o = 16; o > 0; o >>= 1) cand = max(cand, __shfl_xor_sync(0xffffffffu, cand, o));
-    if ((threadIdx.x & 31) == 0) best[threadIdx.x >> 5] = cand;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int bm = -1;
-        for (int w = 0; w < 32; ++w) bm = max(bm, best[w]);
-        bounds[4] = (bm < 0) ? lo : lo + (hi - lo) * (double)(bm + 1) / 1024.0;
+    const int m = blockIdx.x * 32 + threadIdx.x;
+    if (m < 1023) hist[m] = sturm_count(0, n, d, e2, lo + (hi - lo) * (double)(m + 1) / 1024.0, pivmin);
+    if (m == 0) {
+        bounds[5] = 1.0;
+        bounds[6] = (double)kc;
     }
 }
 
@@ -719,7 +715,7 @@ __global__ void __launch_bounds__(1024) k_cut_coarse(int n, int kc, const double
 // by 33-way multisection of the Gershgorin interval; d, e^2 in shared memory
 __global__ void k_bisect(int n, const double* __restrict__ d, const double* __restrict__ e2,
                          const double* __restrict__ bounds, const int* __restrict__ blk,
-                         double* __restrict__ lam) {
+                         double* __restrict__ lam, const int* __restrict__ hist) {
     extern __shared__ double sde[];
     double* sd = sde;
     double* se = sde + n;
@@ -739,7 +735,18 @@ __global__ void k_bisect(int n, const double* __restrict__ d, const double* __re
     const double pivmin = bounds[2];
     double lo = bounds[0], hi = bounds[1];
     // below the cut (only the top eigenvalues are wanted): park at the lower bound
-    if (sturm_count(bs, bt, sd, se, bounds[4], pivmin) > k) {
+    double xcut = -DBL_MAX;
+    if (bounds[5] > 0.5) {  // largest coarse point with count <= kc (k_cut_coarse)
+        const int kc = (int)bounds[6];
+        int a = 0, b = 1023;  // first m with hist[m] > kc (1023: none)
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (hist[mid] > kc) b = mid;
+            else a = mid + 1;
+        }
+        xcut = (a == 0) ? lo : lo + (hi - lo) * (double)a / 1024.0;
+    }
+    if (sturm_count(bs, bt, sd, se, xcut, pivmin) > k) {
         if (lane == 0) lam[p] = lo;
         return;
     }
@@ -1188,7 +1195,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     const size_t n2 = (size_t)n * n;
     wk.V.alloc(n2);
     wk.W.alloc((size_t)n * TRD_NB);
-    wk.vec.alloc((size_t)11 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB * TRD_DSPLIT + 8);
+    wk.vec.alloc((size_t)11 * n + (size_t)SLOTW * wk.grid + 2 * TRD_NB * TRD_DSPLIT + 8 + 512);
     double* d = wk.vec.p;
     double* e = d + n;
     double* tau = e + n;
@@ -1202,6 +1209,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     double* bounds = dots + 2 * TRD_NB * TRD_DSPLIT;
     int* blk = reinterpret_cast<int*>(bounds + 8);       // 2n ints
     int* order = blk + 2 * n;                            // n ints
+    int* hist = order + n;                               // 1024 ints: coarse Sturm counts
     fill_zero(st, wk.V.p, (int64_t)n2);
     fill_zero(st, e, n);
     fill_zero(st, tau, n);
@@ -1274,13 +1282,13 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     note_launch();
     if (nvec < n - 1 && n >= 256) {  // only the top nvec + 1 eigenvalues are needed
         note_launch();
-        k_cut_coarse<<<1, 1024, 0, st>>>(n, n - nvec - 1, d, e2, bounds);
+        k_cut_coarse<<<32, 32, 0, st>>>(n, n - nvec - 1, d, e2, bounds, hist);
         AERO_LAUNCHED();
     } else {
-        const double ninf = -DBL_MAX;
-        AERO_CUDA(cudaMemcpyAsync(bounds + 4, &ninf, sizeof(double), cudaMemcpyHostToDevice, st));
+        const double nocut[3] = {-DBL_MAX, 0.0, 0.0};  // bounds[4..6]: no cut, no coarse counts
+        AERO_CUDA(cudaMemcpyAsync(bounds + 4, nocut, sizeof(nocut), cudaMemcpyHostToDevice, st));
     }
-    k_bisect<<<(n * 32 + 127) / 128, 128, sde, st>>>(n, d, e2, bounds, blk, lam);
+    k_bisect<<<(n * 32 + 127) / 128, 128, sde, st>>>(n, d, e2, bounds, blk, lam, hist);
     AERO_LAUNCHED();
     note_launch();
     k_order<<<(n + 127) / 128, 128, 0, st>>>(n, lam, order, w);
