@@ -836,7 +836,7 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
     double dp = safe(sd[bs] - lv);
     DP(bs) = dp;
     for (int i = bs; i < bt - 1; ++i) {
-        dp = safe(sd[i + 1] - lv - se[i] * (se[i] / dp));
+        dp = safe(sd[i + 1] - lv - (se[i] * se[i]) * rcp_nr(dp));  // reciprocal off the divide path
         DP(i + 1) = dp;
     }
     // numerically repeated eigenvalue (gap to a neighbour < 1e-12 ||T||): a twisted
@@ -943,7 +943,7 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
         for (int u = 0; u < PF; ++u) {
             const int i = ib - u;
             if (i < bs) break;
-            dm = safe(sd[i] - lv - se[i] * (se[i] / dm));
+            dm = safe(sd[i] - lv - (se[i] * se[i]) * rcp_nr(dm));
             ZZ(i) = dm;
             const double g = pre[u] + dm - (sd[i] - lv);
             if (fabs(g) < best) {
