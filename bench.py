@@ -15,6 +15,7 @@ DESIGN.md section 6).
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -56,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--rng", default="device", choices=["device", "host"],
+                    help="random projections drawn on the device, or on the host and uploaded "
+                         "(AERO_FLAG_HOST_RNG: bit-identical to the reference's rng.hpp)")
     return ap.parse_args()
 
 
@@ -149,19 +153,6 @@ def fp64_peak_tflops(torch, dev):
     return best
 
 
-def cpu_oracle_rate(cfg, nrows, threads):
-    """Oracle restatement (oracle/) on the host cores over rows 1..nrows."""
-    from oracle import pyoracle as orc
-    import numpy as np
-    orc.set_threads(threads)
-    rows = orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, 0, 1, nrows)
-    s = orc.AttpState(cfg["d"], cfg["eps"], 1, 1000)
-    t0 = time.perf_counter()
-    s.update_block(rows, np.arange(1, nrows + 1))
-    dt = time.perf_counter() - t0
-    return nrows / dt, dt
-
-
 def reference_literal_flops(ev, d, ell):
     """SURVEY.md section 8(d) F_row: the reference's own flop count per row
     (power-iteration gate, simul_iter doubling calls, FD reduce by SVD, dumps),
@@ -180,6 +171,90 @@ def reference_literal_flops(ev, d, ell):
     red = 2 * (2 * ell) ** 2 * d + 9 * (2 * ell) ** 3 + 2 * (ell - 1) * (2 * ell) * d
     f = f + ev["reduced"].astype(np.float64) * float(red) + 8.0 * r * d * ev["xi"].astype(np.float64)
     return float(f.mean())
+
+
+def attp_cycle(cfg, S, warm, steps):
+    """The first full FD-reduce cycle inside the GPU arm's timed rows: the
+    reduce fires at row 2*ell, then every ell+1 rows (sketch.cpp:92-95,
+    data-independent), so the residual size r -- which sets the per-row cost --
+    is periodic with period ell+1. Returns (first row after a reduce, ell)."""
+    ell = int(math.ceil(2.0 / cfg["eps"]))
+    start = warm * S + 1
+    m = max(0, -(-(start - 1 - 2 * ell) // (ell + 1)))  # reduce rows 2ell + m(ell+1) >= start - 1
+    t_red = 2 * ell + m * (ell + 1)
+    if t_red + ell + 1 > (warm + steps) * S:
+        raise ValueError("timed region shorter than one reduce cycle")
+    return t_red + 1, ell
+
+
+def attp_cpu_sample(cfg, S, warm, steps, threads, points, per_point, warm_points=0, device=0):
+    """Like-for-like CPU timing of the GPU arm's steady-state rows (the oracle
+    restatement, or the reference arm): the GPU engine (untimed setup) replays
+    the same stream up to each sample point, its live state (residual rows,
+    fork counter, clock, last dump time, mass) is imported into the oracle,
+    and the oracle's update() is timed on the next `per_point` rows. The
+    points are spread evenly over one FD-reduce cycle of the timed region
+    (so their mean residual size is the cycle's), plus the cycle's reduce row
+    timed on its own. Rate = (ell+1) / (ell * mean t_row + t_reduce_row)."""
+    import numpy as np
+    import torch
+    import paper_2601_02019_b200 as prod
+    from oracle import pyoracle as orc
+    orc.set_threads(threads)
+    c0, ell = attp_cycle(cfg, S, warm, steps)
+    period = ell + 1
+    xs = [c0 + (i * (period - per_point)) // max(1, points) for i in range(points)]
+    warm_xs = [c0 + (i * (period - per_point)) // max(1, warm_points) for i in range(warm_points)]
+    red_row = c0 + ell  # the cycle's reduce row
+    d = cfg["d"]
+    last = red_row
+    dev = torch.device("cuda", device)
+    rows = torch.empty((last, d), dtype=torch.float64, device=dev)
+    prod.gen_rows_device(rows, 1, d, cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1, stream=0,
+                         device=device)
+    torch.cuda.synchronize(dev)
+    ts = np.arange(1, last + 1, dtype=np.int64)
+    gpu = prod.AttpState(d, cfg["eps"], seed=1, stream=1000, device=device)
+    pos = 0
+    t_rows, t_warm, t_red = [], [], None
+    targets = sorted(set([(x, "w") for x in warm_xs] + [(x, "t") for x in xs] + [(red_row, "r")]))
+    for x, kind in targets:
+        if x - 1 > pos:
+            gpu.update_block(rows[pos:x - 1], ts[pos:x - 1])
+            pos = x - 1
+        inf = gpu.info()
+        res = gpu.residual()
+        o = orc.AttpState(d, cfg["eps"], 1, 1000)
+        o.import_state(res, inf.forks, inf.clock, inf.last_dump_t, inf.theta, inf.fro_mass)
+        n = 1 if kind == "r" else per_point
+        host = rows[x - 1:x - 1 + n].cpu().numpy()
+        t0 = time.perf_counter()
+        ev = o.update_block(host, ts[x - 1:x - 1 + n])
+        dt = time.perf_counter() - t0
+        if kind == "r":
+            assert ev["reduced"][0] == 1, "cycle reduce row did not reduce"
+            t_red = dt
+        elif kind == "t":
+            assert not ev["reduced"].any()
+            t_rows.append(dt / n)
+        else:
+            t_warm.append(dt / n)
+    del gpu, rows
+    torch.cuda.empty_cache()
+    mean_row = float(np.mean(t_rows))
+    rate = period / (ell * mean_row + t_red)
+    sample = (f"{points} points x {per_point} rows spread over the FD-reduce cycle rows {c0}..{red_row} of the "
+              f"GPU arm's timed region (rows {warm * S + 1}..{(warm + steps) * S}) plus that cycle's reduce row, "
+              f"each from the GPU run's exported live state; rate = (ell+1)/(ell*mean_row + reduce_row) with "
+              f"mean_row {mean_row * 1e3:.1f} ms, reduce_row {t_red * 1e3:.0f} ms")
+    return rate, sample, t_rows, t_red
+
+
+def gpu_arm_steps(args):
+    """(warm-up, timed) steps of the GPU arm: the driver launches both arms
+    with the same --steps/--warmup, so the reference arm samples the rows the
+    GPU arm times."""
+    return args.warmup, args.steps
 
 
 def run_reference(args, cfg, rank):
@@ -207,24 +282,20 @@ def run_reference(args, cfg, rank):
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
         return
-    per = max(1, (args.cpu_rows or cfg["cpu_rows"]) // max(1, args.steps + args.warmup))
-    nrows = per * (args.steps + args.warmup)
-    rows = orc.gen_rows(cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], 1, 0, 1, nrows)
-    s = orc.AttpState(cfg["d"], cfg["eps"], 1, 1000)
-    for w in range(args.warmup):
-        s.update_block(rows[w * per:(w + 1) * per], np.arange(w * per + 1, (w + 1) * per + 1))
-    t0 = time.perf_counter()
-    for k in range(args.warmup, args.warmup + args.steps):
-        s.update_block(rows[k * per:(k + 1) * per], np.arange(k * per + 1, (k + 1) * per + 1))
-    dt = time.perf_counter() - t0
-    v = per * args.steps / dt
-    sample = f"rows {args.warmup * per + 1}..{nrows} of the {args.config.upper()} stream (from an empty sketch)"
+    # the GPU arm's config and timed rows; each step = one sample point
+    S = args.rows_per_step or cfg["rows_per_step"]
+    gwarm, gsteps = gpu_arm_steps(args)
+    v, sample, t_rows, t_red = attp_cpu_sample(cfg, S, gwarm, gsteps, threads, points=args.steps,
+                                               per_point=cfg.get("ref_rows_per_point", 2),
+                                               warm_points=args.warmup)
     print(json.dumps({
         "impl": "reference", "metric": "sketch update throughput", "value": v, "unit": "rows/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": float(np.mean(t_rows)) * cfg.get("ref_rows_per_point", 2) * 1e3,
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "rows_per_step": per},
+        "config": {"workload": cfg["name"], "rows_per_step": S, "same_config": True,
+                   "timed_rows": f"{gwarm * S + 1}..{(gwarm + gsteps) * S}"},
         "cpu_baseline": {"value": v, "unit": "rows/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -445,7 +516,8 @@ def main():
             ms = float(t.item())
         return ms, launches, clk.summary(), np.concatenate(evs)
 
-    sk = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local)
+    hr = args.rng == "host"
+    sk = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, host_rng=hr)
     ms, launches, clocks, ev = run(sk)
     info = sk.info()
     value = world * S * steps / (ms * 1e-3)
@@ -454,7 +526,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         host = rows.cpu().pin_memory().numpy()
-        sk2 = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local)
+        sk2 = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, host_rng=hr)
         ms2, _, _, _ = run(sk2, host_rows=host)
         e2e = {"value": world * S * steps / (ms2 * 1e-3), "unit": "rows/s",
                "h2d_bytes_per_step": S * d * 8, "d2h_bytes_per_step": S * ev.dtype.itemsize}
@@ -463,7 +535,7 @@ def main():
     # roofline counters: a third, profiled pass over the same rows (per-launch
     # CUDA events around the product kernels slow the step, so `value` above
     # comes from the unprofiled pass)
-    skp = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, profile=True)
+    skp = prod.AttpState(d, cfg["eps"], seed=1 + rank, stream=1000, device=local, profile=True, host_rng=hr)
     ms_p, _, _, _ = run(skp)
     prof = skp.profile()
     del skp
@@ -472,13 +544,10 @@ def main():
     if rank == 0:
         peak = fp64_peak_tflops(torch, dev)
         achieved = (prof["product_flops"] / max(prof["product_ms"], 1e-9)) / 1e9  # TFLOP/s
+        # DRAM bytes per launch need an ncu capture of THIS launch; a bench run
+        # cannot measure them, so the key is null here and the ncu --set full
+        # numbers live under profiles/ 
         traffic = None
-        summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
-        if os.path.exists(summ):
-            try:
-                traffic = json.load(open(summ)).get("product_dram_bytes_per_launch")
-            except Exception:
-                traffic = None
         i8 = info.ell * 2 >= 1024 and os.environ.get("AERO_PRODUCT_I8", "1") != "0"
         kern = ("k_iterate_i8 (persistent cooperative: every phase of a batch = G.X on the int8 tcgen05 tensor "
                 "cores by exact 7-slice Ozaki splitting, TMEM accumulators, + per-job normalization; kernels.cu, "
@@ -513,12 +582,13 @@ def main():
                          "event log, at the measured fp64 DGEMM peak; the Gram-form engine executes fewer"}
         cpu = None
         if not args.no_cpu:
-            threads = 1
-            n_cpu = args.cpu_rows or cfg["cpu_rows"]
-            rate, dt = cpu_oracle_rate(cfg, n_cpu, threads)
-            cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port",
-                   "sample": f"rows 1..{n_cpu} of the {args.config.upper()} stream from an empty sketch "
-                             f"({dt:.1f} s; oracle restatement over OpenBLAS, 1 thread like the reference)"}
+            threads = 1  # the reference is single-threaded (proj/CMakeLists.txt: no threads/OpenMP)
+            t0 = time.perf_counter()
+            rate, sample, _, _ = attp_cpu_sample(cfg, S, warm, steps, threads, points=cfg.get("cpu_points", 8),
+                                                 per_point=1, device=local)
+            cpu = {"value": rate, "unit": "rows/s", "cores": threads, "kind": "port", "same_config": True,
+                   "sample": sample + f"; oracle restatement over OpenBLAS, 1 thread "
+                                      f"({time.perf_counter() - t0:.0f} s incl. the GPU state replay)"}
         out = {
             "metric": "sketch update throughput", "value": value, "unit": "rows/s", "n_gpus": world,
             "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,

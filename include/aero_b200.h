@@ -36,6 +36,11 @@ extern "C" {
 /* flags */
 #define AERO_FLAG_EXACT 1   /* no speculative row batching (one row per device step) */
 #define AERO_FLAG_PROFILE 2 /* time the batched G.X products with CUDA events */
+/* random projections from the host: the start vectors of every power_iteration
+ * and the Pi of every simul_iter are drawn on the host by this library's
+ * restatement of rng.hpp:54-78 (host libm) and uploaded, instead of being drawn
+ * on the device (see aero_set_rng_fill for a caller-owned source) */
+#define AERO_FLAG_HOST_RNG 4
 
 typedef struct aero_sketch aero_sketch; /* opaque AeroState / AttpState */
 
@@ -83,13 +88,27 @@ int aero_create(const aero_cfg* cfg, aero_sketch** out);
 int aero_destroy(aero_sketch* h);
 /* AeroState::set_theta (sketch.cpp:33-36) */
 int aero_set_theta(aero_sketch* h, double theta);
+/* Caller-owned random projections (north star: "projection
+ * matrices passed in through the FFI"). The sketch consumes one RngState fork
+ * per power_iteration (sketch.cpp:99, linalg.cpp:106-108: first r Gaussians)
+ * and per simul_iter (sketch.cpp:53, linalg.cpp:141: the r x k Pi, row-major,
+ * i.e. the first r*k Gaussians). The library asks for them as
+ *   fill(ctx, n, out, count): out[0..count) = the first `count` Gaussians of
+ *   fork #n (n >= 1) of the sketch's RngState(seed, stream) (rng.hpp:54-57),
+ * returning 0 on success (nonzero -> AERO_INVALID_INPUT from the update).
+ * fill is called from library threads, concurrently for distinct forks.
+ * fn == NULL reverts to the default (device draws, or AERO_FLAG_HOST_RNG). */
+typedef int (*aero_rng_fill)(void* ctx, uint64_t fork_index, double* out, int64_t count);
+int aero_set_rng_fill(aero_sketch* h, aero_rng_fill fn, void* ctx);
 /* n sequential AeroState::update / AttpState::update calls (sketch.cpp:82-141,
  * attp.hpp:21-26). t: n strictly increasing timestamps > clock. theta_per_row
  * (nullable, fixed mode only) sets the threshold before each row. log_out
  * (nullable) receives one aero_event per row. */
 int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
                       const double* theta_per_row, aero_event* log_out);
-/* same, rows already resident in device memory (ld in elements) */
+/* same, rows already resident in device memory (ld in elements). The rows
+ * are read on aero_stream(h): the caller must order their producer before it
+ * (cudaStreamWaitEvent on aero_stream(h), or a completed producer stream). */
 int aero_update_block_device(aero_sketch* h, const double* rows_device, int64_t n, int64_t ld,
                              const int64_t* t, const double* theta_per_row, aero_event* log_out);
 /* AeroState::query(lb, ub) (sketch.cpp:143-160): ell x d row-major */
@@ -242,6 +261,9 @@ int aero_dev_product(int32_t r, int32_t n, const double* g, const double* x, con
 /* RngState draws on the device (test hook): count gaussians of fork #fork of
  * RngState(seed, stream) (fork 0 = the root), to host memory */
 int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out);
+/* the same draws by the host restatement AERO_FLAG_HOST_RNG uses (rng.hpp:60-78
+ * with the host libm; needs no GPU) */
+int aero_rng_gaussians_host(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out);
 
 #ifdef __cplusplus
 }

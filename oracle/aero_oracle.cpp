@@ -379,13 +379,33 @@ int power_iter_count(int d) {
 }
 
 // reference sketch.cpp:22-31
-AeroState::AeroState(int d, double eps, double theta, RngState rng)
+AeroState::AeroState(int d, double eps, double theta, RngState rng, double delta)
     : d_(d), eps_(eps), ell_(0), theta_(theta), eps_si_(0.4), ct_(Mat(d > 0 ? d : 0, 0)),
       clock_(0), last_dump_t_(0), rng_(rng) {
     if (d < 1) throw InvalidInput("AeroState: d must be >= 1");
     if (!(eps > 0.0 && eps <= 1.0)) throw InvalidInput("AeroState: eps out of (0,1]");
     if (theta < 0.0) throw InvalidInput("AeroState: theta must be >= 0");
+    if (delta != 0.0 && !(delta > 0.0 && delta < 1.0)) throw InvalidInput("AeroState: delta out of (0, 1)");
+    delta_ = delta;
     ell_ = static_cast<int>(std::ceil(2.0 / eps));
+}
+
+// reference sketch.cpp:45-48
+void AeroState::update_amplified(const double* a, std::int64_t i) {
+    if (delta_ == 0.0) throw InvalidInput("AeroState: amplification requested without delta");
+    update_impl(a, i, true);
+}
+
+void AeroState::import_state(const double* rows_rm, std::int64_t r, std::uint64_t forks, std::int64_t clock,
+                             std::int64_t last_dump_t, double theta) {
+    if (r < 0 || r > 2 * (std::int64_t)ell_) throw InvalidInput("import_state: rows out of range");
+    ct_ = Mat(d_, r);
+    std::copy(rows_rm, rows_rm + r * d_, ct_.v.begin());  // C row-major == C^T column-major
+    snaps_.clear();
+    rng_.set_forks(forks);
+    clock_ = clock;
+    last_dump_t_ = last_dump_t;
+    theta_ = theta;
 }
 
 void AeroState::set_theta(double theta) {
@@ -393,15 +413,45 @@ void AeroState::set_theta(double theta) {
     theta_ = theta;
 }
 
-// reference sketch.cpp:50-54 (non-amplified branch only; delta is in no config)
-SimulIterResult AeroState::factorize(const Mat& at, int k) {
-    ++stats_.simul_calls;
-    return simul_iter(at, k, eps_si_, rng_.fork());
+// reference sketch.cpp:50-80: plain simul_iter, or r candidates at eps_si=0.2
+// whose residual C'^T - z z^T C'^T is scored by the max of s power
+// iterations; the smallest score wins (the first on ties)
+SimulIterResult AeroState::factorize(const Mat& at, int k, bool amplified) {
+    if (!amplified) {
+        ++stats_.simul_calls;
+        return simul_iter(at, k, eps_si_, rng_.fork());
+    }
+    const double delta = delta_;
+    const int r = static_cast<int>(std::ceil(std::log(2.0 / delta) / std::log(100.0)));
+    if (r <= 1) {
+        ++stats_.simul_calls;
+        return simul_iter(at, k, 0.2, rng_.fork());
+    }
+    const int s = static_cast<int>(std::ceil(2.0 * std::log(2.0 / delta) / std::log(3.0)));
+    const int kp = power_iter_count(d_);
+    SimulIterResult best;
+    double best_cost = 0.0;
+    for (int h = 0; h < r; ++h) {
+        ++stats_.simul_calls;
+        SimulIterResult cand = simul_iter(at, k, 0.2, rng_.fork());
+        // at_res = at - z (z^T at)   (d x r)
+        const Mat zt_at = matmul(cand.z, at, true, false);   // k x r
+        const Mat proj = matmul(cand.z, zt_at, false, false);  // d x r
+        Mat at_res = at;
+        for (std::int64_t q = 0; q < at_res.size(); ++q) at_res.v[q] -= proj.v[q];
+        double cost = 0.0;
+        for (int rep = 0; rep < s; ++rep) cost = std::max(cost, power_iteration(at_res, kp, rng_.fork()).first);
+        if (h == 0 || cost < best_cost) {
+            best_cost = cost;
+            best = std::move(cand);
+        }
+    }
+    return best;
 }
 
 // reference sketch.cpp:82-141. The buffer is held as C'^T (d x r, column-major)
 // which is C' in row-major order; every product below is the reference's.
-void AeroState::update(const double* a, std::int64_t i) {
+void AeroState::update_impl(const double* a, std::int64_t i, bool amplified) {
     if (!all_finite(a, d_)) throw InvalidInput("AeroState: non-finite row");
     if (i <= clock_) throw InvalidInput("AeroState: timestamp regression");
     stats_ = UpdateStats{};
@@ -436,7 +486,7 @@ void AeroState::update(const double* a, std::int64_t i) {
         int k = std::min(2, kmax);
         while (true) {
             ++stats_.doubling_steps;
-            const SimulIterResult fac = factorize(cp, k);
+            const SimulIterResult fac = factorize(cp, k, amplified);
             const double tail = fac.sigma_hat[k - 1] * fac.sigma_hat[k - 1];
             ev_.k_last = k;
             ev_.tail_sq = tail;
@@ -533,7 +583,8 @@ Mat shrink_to_sketch(const Mat& b, int ell) {
 void AttpState::update(const double* a, std::int64_t i) {
     fro_mass_ += sq_norm(a, inner_.d());
     inner_.set_theta(inner_.eps() * fro_mass_);
-    inner_.update(a, i);
+    if (inner_.delta() != 0.0) inner_.update_amplified(a, i);  // attp.hpp:24
+    else inner_.update(a, i);
 }
 Mat AttpState::query(std::int64_t t) const {
     if (t < 1 || t > inner_.clock()) throw InvalidInput("AttpState: t out of range");
@@ -542,7 +593,7 @@ Mat AttpState::query(std::int64_t t) const {
 
 // ---------------------------------------------------------------- sliding window
 // reference sliding_window.cpp:15-30
-MlState::MlState(int d, std::int64_t n, double r_max, double eps, RngState rng)
+MlState::MlState(int d, std::int64_t n, double r_max, double eps, RngState rng, double delta)
     : d_(d), n_(n), r_max_(r_max), eps_(eps), ell_(0), cap_(0), clock_(0), window_mass_(0.0),
       norm_warnings_(0) {
     if (n < 1) throw InvalidInput("MlState: window size must be >= 1");
@@ -553,7 +604,7 @@ MlState::MlState(int d, std::int64_t n, double r_max, double eps, RngState rng)
     const int big_l = static_cast<int>(std::ceil(std::log2(std::max(r_max, 2.0))));
     for (int j = 0; j < std::max(big_l, 1); ++j) {
         const double theta_j = std::pow(2.0, j) * eps * static_cast<double>(n);
-        levels_.emplace_back(d, eps, theta_j, rng.fork());
+        levels_.emplace_back(d, eps, theta_j, rng.fork(), delta);
         heavy_.emplace_back();
     }
 }
@@ -605,7 +656,8 @@ void MlState::update(const double* a, std::int64_t i) {
         if (nsq >= levels_[j].theta()) {
             heavy_[j].push_back(HeavyRow{Vec(a, a + d_), tail_t(j) + 1, i});
         } else {
-            levels_[j].update(a, i);
+            if (levels_[j].delta() != 0.0) levels_[j].update_amplified(a, i);  // sliding_window.cpp:90-91
+            else levels_[j].update(a, i);
         }
         while (combined_len(j) > cap_) pop_front(j);
     }

@@ -72,6 +72,9 @@ class RngState {
     std::uint64_t seed() const { return seed_; }
     std::uint64_t stream() const { return stream_; }
     std::uint64_t forks() const { return forks_; }
+    // state import (bench like-for-like timing): a parent that so far only
+    // forked is fully described by (seed, stream, forks)
+    void set_forks(std::uint64_t n) { forks_ = n; }
     RngState fork() {
         ++forks_;
         return RngState(seed_, mix64(stream_ ^ mix64(forks_)));
@@ -171,8 +174,12 @@ int power_iter_count(int d);
 
 class AeroState {
   public:
-    AeroState(int d, double eps, double theta, RngState rng);
-    void update(const double* a, std::int64_t i);
+    // delta > 0 enables probability amplification (sketch.hpp:44-46; 0 = none)
+    AeroState(int d, double eps, double theta, RngState rng, double delta = 0.0);
+    void update(const double* a, std::int64_t i) { update_impl(a, i, false); }
+    // sketch.cpp:45-48
+    void update_amplified(const double* a, std::int64_t i);
+    double delta() const { return delta_; }
     Mat query(std::int64_t lb, std::int64_t ub) const;
     Mat query_gram(std::int64_t lb, std::int64_t ub) const;  // pre-shrink B
     int d() const { return d_; }
@@ -192,9 +199,17 @@ class AeroState {
     std::int64_t last_dump_time() const { return last_dump_t_; }
     std::uint64_t forks() const { return rng_.forks(); }
     double eps_si() const { return eps_si_; }
+    // Replace the live state by an exported one (the GPU engine's residual
+    // rows, fork counter, clock, last dump time and threshold) so that the
+    // CPU baseline times the SAME steady-state rows as the GPU run. The
+    // snapshot queue is left empty: update() never reads it (sketch.cpp:82-141).
+    void import_state(const double* rows_rm, std::int64_t r, std::uint64_t forks, std::int64_t clock,
+                      std::int64_t last_dump_t, double theta);
 
   private:
-    SimulIterResult factorize(const Mat& at, int k);
+    void update_impl(const double* a, std::int64_t i, bool amplified);
+    SimulIterResult factorize(const Mat& at, int k, bool amplified);
+    double delta_ = 0.0;
     int d_;
     double eps_;
     int ell_;
@@ -217,13 +232,15 @@ Mat shrink_to_sketch(const Mat& b, int ell);
 // ---- attp (reference attp.hpp:15-43) -----------------------------------------
 class AttpState {
   public:
-    AttpState(int d, double eps, RngState rng) : inner_(d, eps, 0.0, rng), fro_mass_(0.0) {}
+    AttpState(int d, double eps, RngState rng, double delta = 0.0)
+        : inner_(d, eps, 0.0, rng, delta), fro_mass_(0.0) {}
     void update(const double* a, std::int64_t i);
     Mat query(std::int64_t t) const;
     double fro_mass() const { return fro_mass_; }
     std::int64_t clock() const { return inner_.clock(); }
     const AeroState& inner() const { return inner_; }
     AeroState& inner() { return inner_; }
+    void set_fro_mass(double m) { fro_mass_ = m; }
 
   private:
     AeroState inner_;
@@ -241,7 +258,7 @@ struct MlQueryResult {
 };
 class MlState {
   public:
-    MlState(int d, std::int64_t n, double r_max, double eps, RngState rng);
+    MlState(int d, std::int64_t n, double r_max, double eps, RngState rng, double delta = 0.0);
     void update(const double* a, std::int64_t i);
     MlQueryResult query() const;
     int d() const { return d_; }

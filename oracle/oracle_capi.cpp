@@ -141,6 +141,34 @@ void* orc_aero_create(int d, double eps, double theta, std::uint64_t seed, std::
         return nullptr;
     return p;
 }
+void* orc_aero_create2(int d, double eps, double theta, std::uint64_t seed, std::uint64_t stream, double delta) {
+    AeroState* p = nullptr;
+    if (guard([&] { p = new AeroState(d, eps, theta, RngState(seed, stream), delta); }) != 0)
+        return nullptr;
+    return p;
+}
+int orc_aero_update_block_amplified(void* h, const double* rows, std::int64_t n, const std::int64_t* t,
+                                    const double* theta, Event* ev) {
+    return guard([&] {
+        auto* s = static_cast<AeroState*>(h);
+        for (std::int64_t q = 0; q < n; ++q) {
+            if (theta) s->set_theta(theta[q]);
+            s->update_amplified(rows + q * s->d(), t[q]);
+            if (ev) ev[q] = s->last_event();
+        }
+    });
+}
+void* orc_attp_create2(int d, double eps, std::uint64_t seed, std::uint64_t stream, double delta) {
+    AttpState* p = nullptr;
+    if (guard([&] { p = new AttpState(d, eps, RngState(seed, stream), delta); }) != 0) return nullptr;
+    return p;
+}
+void* orc_ml_create2(int d, std::int64_t n, double rmax, double eps, std::uint64_t seed, std::uint64_t stream,
+                     double delta) {
+    MlState* p = nullptr;
+    if (guard([&] { p = new MlState(d, n, rmax, eps, RngState(seed, stream), delta); }) != 0) return nullptr;
+    return p;
+}
 void orc_aero_destroy(void* h) { delete static_cast<AeroState*>(h); }
 int orc_aero_set_theta(void* h, double th) {
     return guard([&] { static_cast<AeroState*>(h)->set_theta(th); });
@@ -229,6 +257,14 @@ int orc_attp_query(void* h, std::int64_t t, double* out) {
     return guard([&] { to_rm(static_cast<AttpState*>(h)->query(t), out); });
 }
 double orc_attp_mass(void* h) { return static_cast<AttpState*>(h)->fro_mass(); }
+int orc_attp_import(void* h, const double* rows, std::int64_t r, std::uint64_t forks, std::int64_t clock,
+                    std::int64_t last_dump_t, double theta, double fro_mass) {
+    return guard([&] {
+        auto* s = static_cast<AttpState*>(h);
+        s->inner().import_state(rows, r, forks, clock, last_dump_t, theta);
+        s->set_fro_mass(fro_mass);
+    });
+}
 void* orc_attp_inner(void* h) { return &static_cast<AttpState*>(h)->inner(); }
 
 // ---- MlState

@@ -104,6 +104,10 @@ def _declare(L):
     d("orc_shrink_to_sketch", i32, dp, i32, i32, dp)
     d("orc_restore_contribution", i32, dp, dp, i32, i32, dp)
     d("orc_aero_create", vp, i32, f64, f64, u64, u64)
+    d("orc_aero_create2", vp, i32, f64, f64, u64, u64, f64)
+    d("orc_aero_update_block_amplified", i32, vp, dp, i64, lp, dp, P(Event))
+    d("orc_attp_create2", vp, i32, f64, u64, u64, f64)
+    d("orc_ml_create2", vp, i32, i64, f64, f64, u64, u64, f64)
     d("orc_aero_destroy", None, vp)
     d("orc_aero_set_theta", i32, vp, f64)
     d("orc_aero_update_block", i32, vp, dp, i64, lp, dp, P(Event))
@@ -121,6 +125,7 @@ def _declare(L):
     d("orc_attp_update_block", i32, vp, dp, i64, lp, P(Event))
     d("orc_attp_query", i32, vp, i64, dp)
     d("orc_attp_mass", f64, vp)
+    d("orc_attp_import", i32, vp, dp, i64, u64, i64, i64, f64, f64)
     d("orc_attp_inner", vp, vp)
     d("orc_ml_create", vp, i32, i64, f64, f64, u64, u64)
     d("orc_ml_destroy", None, vp)
@@ -277,11 +282,11 @@ def restore_contribution(z, m):
 class AeroState:
     """reference sketch.hpp:42-99 (non-amplified)."""
 
-    def __init__(self, d, eps, theta, seed=0, stream=0, _handle=None, _owner=None):
+    def __init__(self, d, eps, theta, seed=0, stream=0, delta=None, _handle=None, _owner=None):
         if _handle is not None:
             self._h, self._own, self._owner = _handle, False, _owner
         else:
-            h = lib().orc_aero_create(d, eps, theta, seed, stream)
+            h = lib().orc_aero_create2(d, eps, theta, seed, stream, float(delta or 0.0))
             if not h:
                 raise InvalidInput(lib().orc_last_error().decode())
             self._h, self._own = h, True
@@ -335,6 +340,22 @@ class AeroState:
         _chk(lib().orc_aero_update_block(self._h, _dp(rows), n, _lp(ts), th, ev))
         return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
 
+    def update_block_amplified(self, rows, ts, thetas=None):
+        """n sequential update_amplified calls (sketch.cpp:45-48)."""
+        rows = _f64(rows)
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = rows.shape[0]
+        ev = (Event * max(n, 1))()
+        th = None
+        if thetas is not None:
+            thetas = _f64(thetas)
+            th = _dp(thetas)
+        _chk(lib().orc_aero_update_block_amplified(self._h, _dp(rows), n, _lp(ts), th, ev))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
+
+    def update_amplified(self, a, i):
+        return self.update_block_amplified(np.asarray(a, np.float64)[None, :], [i])[0]
+
     def query(self, lb, ub):
         out = np.empty((self.ell, self.d))
         _chk(lib().orc_aero_query(self._h, lb, ub, _dp(out)))
@@ -371,8 +392,8 @@ class AeroState:
 class AttpState:
     """reference attp.hpp:15-43."""
 
-    def __init__(self, d, eps, seed=0, stream=0):
-        h = lib().orc_attp_create(d, eps, seed, stream)
+    def __init__(self, d, eps, seed=0, stream=0, delta=None):
+        h = lib().orc_attp_create2(d, eps, seed, stream, float(delta or 0.0))
         if not h:
             raise InvalidInput(lib().orc_last_error().decode())
         self._h = h
@@ -406,6 +427,13 @@ class AttpState:
     def fro_mass(self):
         return lib().orc_attp_mass(self._h)
 
+    def import_state(self, residual, forks, clock, last_dump_t, theta, fro_mass):
+        """Adopt an exported live state (residual rows r x d, RngState fork
+        counter, clock, last dump time, threshold, running mass)."""
+        residual = _f64(residual).reshape(-1, self.d)
+        _chk(lib().orc_attp_import(self._h, _dp(residual), residual.shape[0], int(forks), int(clock),
+                                   int(last_dump_t), float(theta), float(fro_mass)))
+
     @property
     def clock(self):
         return self.inner.clock
@@ -414,8 +442,8 @@ class AttpState:
 class MlState:
     """reference sliding_window.hpp:39-81."""
 
-    def __init__(self, d, n, r_max, eps, seed=0, stream=0):
-        h = lib().orc_ml_create(d, n, r_max, eps, seed, stream)
+    def __init__(self, d, n, r_max, eps, seed=0, stream=0, delta=None):
+        h = lib().orc_ml_create2(d, n, r_max, eps, seed, stream, float(delta or 0.0))
         if not h:
             raise InvalidInput(lib().orc_last_error().decode())
         self._h, self.d, self.n = h, d, n

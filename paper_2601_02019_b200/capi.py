@@ -24,6 +24,7 @@ P = C.POINTER
 AERO_THETA_FIXED, AERO_THETA_ATTP = 0, 1
 AERO_FLAG_EXACT = 1
 AERO_FLAG_PROFILE = 2
+AERO_FLAG_HOST_RNG = 4
 
 
 class InvalidInput(ValueError):
@@ -107,6 +108,7 @@ SIGNATURES = [
     ("aero_create", i32, [P(Cfg), P(vp)]),
     ("aero_destroy", i32, [vp]),
     ("aero_set_theta", i32, [vp, f64]),
+    ("aero_set_rng_fill", i32, [vp, vp, vp]),
     ("aero_update_block", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_update_block_device", i32, [vp, vp, i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_query", i32, [vp, i64, i64, P(f64)]),
@@ -156,6 +158,7 @@ SIGNATURES = [
     ("aero_last_error", C.c_char_p, []),
     ("aero_version", C.c_char_p, []),
     ("aero_kernel_launches", i64, []),
+    ("aero_rng_gaussians_host", i32, [u64, u64, i64, i64, P(f64)]),
     ("aero_rng_gaussians", i32, [u64, u64, i64, i64, P(f64)]),
     ("aero_eigh", i32, [i32, P(f64), P(f64), P(f64), P(f64)]),
     ("aero_dev_product", i32, [i32, i32, P(f64), P(f64), P(i32), i32, P(f64), P(f64)]),
@@ -206,6 +209,13 @@ def rng_gaussians(seed, stream, fork, count):
     return out
 
 
+def rng_gaussians_host(seed, stream, fork, count):
+    """Host draws of AERO_FLAG_HOST_RNG (no GPU needed)."""
+    out = np.empty(count)
+    _chk(lib().aero_rng_gaussians_host(seed, stream, fork, count, _dp(out)))
+    return out
+
+
 def eigh(b, return_ms=False):
     """Device symmetric eigensolver (linalg.cpp:60-77 semantics)."""
     b = _f64(b)
@@ -232,26 +242,55 @@ def dev_product(g, x, colmask=None, mode=0, return_ms=False):
     return (y.T, ms.value) if return_ms else y.T
 
 
-def _device_ptr(x):
-    """(pointer, ld) of a CUDA torch tensor of shape (n, d), float64."""
+def _device_ptr(x, stream_handle=None):
+    """(pointer, ld) of a CUDA torch tensor of shape (n, d), float64.
+
+    The library reads device rows on its own stream; the rows may still be in
+    flight on the caller's current torch stream, so the library stream is
+    made to wait for it (an event, no host sync) when its handle is known,
+    and the caller's stream is synchronized otherwise."""
     import torch
-    assert x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.stride(1) == 1
+    if not (x.is_cuda and x.dtype == torch.float64 and x.dim() == 2 and x.stride(1) == 1):
+        raise InvalidInput("device rows must be a CUDA float64 (n, d) tensor with unit column stride")
+    cur = torch.cuda.current_stream(x.device)
+    if stream_handle:
+        torch.cuda.ExternalStream(stream_handle, device=x.device).wait_stream(cur)
+    else:
+        cur.synchronize()
     return C.c_void_p(x.data_ptr()), x.stride(0)
+
+
+def _check_block(n_rows, n, thetas=None):
+    """rows / thetas must cover exactly the n timestamps (the C side reads n of each)."""
+    if n_rows != n:
+        raise InvalidInput(f"row block has {n_rows} rows for {n} timestamps")
+    if thetas is not None and len(thetas) != n:
+        raise InvalidInput(f"{len(thetas)} thresholds for {n} timestamps")
+
+
+# aero_rng_fill(ctx, fork_index, out, count) (include/aero_b200.h)
+RNG_FILL = C.CFUNCTYPE(i32, vp, u64, P(f64), i64)
 
 
 class AeroState:
     """reference AeroState (sketch.hpp:42-99): construct with d and eps (or an
-    explicit ell), update by row or row block, query(lb, ub)."""
+    explicit ell), update by row or row block, query(lb, ub).
+
+    host_rng=True draws every random projection on the host (the library's
+    restatement of rng.hpp, AERO_FLAG_HOST_RNG); set_rng_fill(fn) hands them to
+    a caller-owned source instead."""
 
     def __init__(self, d, eps, theta=0.0, seed=0, stream=0, device=0, ell=0, theta_mode=AERO_THETA_FIXED,
-                 exact=False, max_batch=0, profile=False, _handle=None, _owner=None):
+                 exact=False, max_batch=0, profile=False, host_rng=False, _handle=None, _owner=None):
         self._owner = _owner
+        self._rng_cb = None
         if _handle is not None:
             self._h, self._own = _handle, False
         else:
             cfg = Cfg(d=d, ell=ell, eps=eps, theta=theta, eps_si=0.0, seed=seed, stream=stream,
                       device=device, theta_mode=theta_mode,
-                      flags=(AERO_FLAG_EXACT if exact else 0) | (AERO_FLAG_PROFILE if profile else 0),
+                      flags=(AERO_FLAG_EXACT if exact else 0) | (AERO_FLAG_PROFILE if profile else 0)
+                      | (AERO_FLAG_HOST_RNG if host_rng else 0),
                       max_batch=max_batch)
             h = vp()
             _chk(lib().aero_create(C.byref(cfg), C.byref(h)))
@@ -294,6 +333,27 @@ class AeroState:
     def set_theta(self, theta):
         _chk(lib().aero_set_theta(self._h, theta))
 
+    def set_rng_fill(self, fn):
+        """fn(fork_index, count) -> the first `count` Gaussians of fork
+        #fork_index of the sketch's RngState (aero_set_rng_fill); None reverts."""
+        if fn is None:
+            self._rng_cb = None
+            _chk(lib().aero_set_rng_fill(self._h, None, None))
+            return
+
+        def tramp(_ctx, fork, out, count):
+            try:
+                vals = np.asarray(fn(int(fork), int(count)), np.float64)
+                if vals.shape != (count,):
+                    return 1
+                C.memmove(out, vals.ctypes.data, 8 * count)
+                return 0
+            except Exception:
+                return 1
+
+        self._rng_cb = RNG_FILL(tramp)  # kept alive as long as the sketch
+        _chk(lib().aero_set_rng_fill(self._h, C.cast(self._rng_cb, vp), None))
+
     def update_block(self, rows, ts, thetas=None):
         """n sequential updates (sketch.cpp:82-141); returns the event log."""
         ts = np.ascontiguousarray(ts, np.int64)
@@ -301,14 +361,16 @@ class AeroState:
         ev = (Event * max(n, 1))()
         th = _f64(thetas) if thetas is not None else None
         if hasattr(rows, "is_cuda") and rows.is_cuda:
-            ptr, ld = _device_ptr(rows)
-            if rows.shape[1] != self.d:
+            if rows.dim() != 2 or rows.shape[1] != self.d:
                 raise InvalidInput("AeroState: row dimension mismatch")
+            _check_block(rows.shape[0], n, th)
+            ptr, ld = _device_ptr(rows, self.stream_handle())
             _chk(lib().aero_update_block_device(self._h, ptr, n, ld, _lp(ts), _dp(th), ev))
         else:
             rows = _f64(rows)
             if rows.ndim != 2 or rows.shape[1] != self.d:
                 raise InvalidInput("AeroState: row dimension mismatch")
+            _check_block(rows.shape[0], n, th)
             _chk(lib().aero_update_block(self._h, _dp(rows), n, self.d, _lp(ts), _dp(th), ev))
         return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
 
@@ -380,9 +442,10 @@ class AeroState:
 class AttpState(AeroState):
     """reference AttpState (attp.hpp:15-43): theta = eps * running mass."""
 
-    def __init__(self, d, eps, seed=0, stream=0, device=0, exact=False, max_batch=0, profile=False):
+    def __init__(self, d, eps, seed=0, stream=0, device=0, exact=False, max_batch=0, profile=False,
+                 host_rng=False):
         super().__init__(d, eps, 0.0, seed, stream, device, theta_mode=AERO_THETA_ATTP,
-                         exact=exact, max_batch=max_batch, profile=profile)
+                         exact=exact, max_batch=max_batch, profile=profile, host_rng=host_rng)
 
     @property
     def inner(self):
@@ -432,12 +495,16 @@ class MlState:
     def update_block(self, rows, ts):
         ts = np.ascontiguousarray(ts, np.int64)
         if hasattr(rows, "is_cuda") and rows.is_cuda:
+            if rows.dim() != 2 or rows.shape[1] != self.d:
+                raise InvalidInput("MlState: row dimension mismatch")
+            _check_block(rows.shape[0], ts.shape[0])
             ptr, ld = _device_ptr(rows)
             _chk(lib().aero_ml_update_block_device(self._h, ptr, ts.shape[0], ld, _lp(ts)))
         else:
             rows = _f64(rows)
             if rows.ndim != 2 or rows.shape[1] != self.d:
                 raise InvalidInput("MlState: row dimension mismatch")
+            _check_block(rows.shape[0], ts.shape[0])
             _chk(lib().aero_ml_update_block(self._h, _dp(rows), rows.shape[0], self.d, _lp(ts)))
 
     def update(self, a, i):
@@ -501,6 +568,8 @@ class CodState:
             raise InvalidInput("CodState: dimension mismatch")
         ts = np.ascontiguousarray(ts, np.int64)
         n = ts.shape[0]
+        _check_block(xs.shape[0], n)
+        _check_block(ys.shape[0], n)
         ev = (Event * max(n, 1))()
         _chk(lib().aero_cod_update_block(self._h, _dp(xs), _dp(ys), n, _lp(ts), ev))
         return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()

@@ -110,4 +110,15 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch, unsign
     __syncthreads();
 }
 
+// grid barrier for kernels whose next phase reads, through the async proxy
+// (cp.async.bulk), data this phase wrote with generic stores (k_iterate_i8):
+// every thread orders its generic writes (global and shared) before the async
+// proxy ahead of the release, and the acquiring thread fences again before its
+// CTA issues bulk copies
+__device__ __forceinline__ void grid_sync_async(unsigned* ctr, unsigned& epoch, unsigned nblocks) {
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+    grid_sync(ctr, epoch, nblocks);
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+}
+
 }  // namespace aero_b200

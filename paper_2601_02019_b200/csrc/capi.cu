@@ -7,6 +7,7 @@
 #include "aero_common.cuh"
 #include "engines.hpp"
 #include "sketch.hpp"
+#include "rng_panels.hpp"
 
 using namespace aero_b200;
 
@@ -80,6 +81,10 @@ int aero_destroy(aero_sketch* h) {
 int aero_set_theta(aero_sketch* h, double theta) {
     REQ(h);
     return guard([&] { h->s->set_theta(theta); });
+}
+int aero_set_rng_fill(aero_sketch* h, aero_rng_fill fn, void* ctx) {
+    REQ(h);
+    return guard([&] { h->s->set_rng_source(h->s->host_rng_default(), fn, ctx); });
 }
 int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
                       const double* theta_per_row, aero_event* log_out) {
@@ -281,6 +286,15 @@ int aero_rng_gaussians(uint64_t seed, uint64_t stream, int64_t fork, int64_t cou
         gen_gaussian_matrix(0, rng_state0(seed, s), count, d);
         AERO_CUDA(cudaMemcpy(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost));
         cudaFree(d);
+    });
+}
+
+int aero_rng_gaussians_host(uint64_t seed, uint64_t stream, int64_t fork, int64_t count, double* out) {
+    REQ(out);
+    return guard([&] {
+        const uint64_t s = (fork > 0) ? fork_stream(stream, (uint64_t)fork) : stream;
+        const uint64_t s0 = rng_state0(seed, s);
+        for (int64_t i = 0; i < count; ++i) out[i] = host_gaussian_at(s0, (uint64_t)i);
     });
 }
 

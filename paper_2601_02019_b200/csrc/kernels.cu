@@ -352,7 +352,8 @@ void eigh_small(cudaStream_t st, int n, double* A, int lda, double* w, int batch
 // batched power / subspace iteration engine (gate K2 + simul_iter K4)
 // ============================================================================
 __global__ void k_iter_init(const IterJob* __restrict__ jobs, const double* __restrict__ G, int ldg,
-                            double* __restrict__ X, int ldx, int R, int* __restrict__ status) {
+                            double* __restrict__ X, int ldx, int R, int* __restrict__ status,
+                            const double* __restrict__ panel) {
     __shared__ double red[32];
     const IterJob jb = jobs[blockIdx.x];
     double tr = 0.0;
@@ -361,11 +362,14 @@ __global__ void k_iter_init(const IterJob* __restrict__ jobs, const double* __re
     const bool zero = (tr == 0.0);
     if (threadIdx.x == 0) status[blockIdx.x] = zero ? JOB_ZERO : JOB_ACTIVE;
     double ss = 0.0;
+    const double* pj = (panel && jb.panel >= 0) ? panel + jb.panel : nullptr;
     for (int j = 0; j < jb.k; ++j) {
         double* x = X + (int64_t)(jb.col + j) * ldx;
         for (int i = threadIdx.x; i < R; i += blockDim.x) {
             double v = 0.0;
-            if (i < jb.r && !zero) v = rng_gaussian_at(jb.rng0, (uint64_t)i * jb.k + j);
+            // Pi is r x k row-major in draw order (linalg.cpp:141, gaussian_matrix)
+            if (i < jb.r && !zero)
+                v = pj ? pj[(int64_t)i * jb.k + j] : rng_gaussian_at(jb.rng0, (uint64_t)i * jb.k + j);
             x[i] = v;
             ss = fma(v, v, ss);
         }
@@ -379,9 +383,9 @@ __global__ void k_iter_init(const IterJob* __restrict__ jobs, const double* __re
     }
 }
 void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg,
-               double* X, int ldx, int R, int* status) {
+               double* X, int ldx, int R, int* status, const double* panel) {
     if (njobs <= 0) return;
-    k_iter_init<<<njobs, 256, 0, st>>>(jobs, G, ldg, X, ldx, R, status);
+    k_iter_init<<<njobs, 256, 0, st>>>(jobs, G, ldg, X, ldx, R, status, panel);
     AERO_LAUNCHED();
 }
 
@@ -858,7 +862,7 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
             __syncthreads();
         }
     }
-    grid_sync(a.bar, epoch, G);
+    grid_sync_async(a.bar, epoch, G);
     // this CTA's first job, read once (jobs are fixed for the whole launch)
     const IterJob jb0 = ((int)blockIdx.x < a.njobs) ? a.jobs[blockIdx.x] : IterJob{};
     const bool pr = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
@@ -881,7 +885,7 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
                           a.ws + z * sstride, R, nullptr, 0, sm, tmem);
         }
         I8_MARK(0);
-        grid_sync(a.bar, epoch, G);
+        grid_sync_async(a.bar, epoch, G);
         I8_MARK(1);
         for (int j = blockIdx.x; j < a.njobs; j += G) {
             const IterJob jb = (j == (int)blockIdx.x) ? jb0 : a.jobs[j];
@@ -893,7 +897,7 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
             if (j == 0) I8_MARK(4);
         }
         I8_MARK(2);
-        grid_sync(a.bar, epoch, G);
+        grid_sync_async(a.bar, epoch, G);
         I8_MARK(3);
     }
 #undef I8_MARK

@@ -64,16 +64,18 @@ struct IterJob {
     int k;          // columns (1 for gate)
     int col;        // first column in the X / Y work arrays
     int nphase;     // number of G products: kp + 1 (gate) or q + 1 (simul)
-    int pad;
+    int panel;      // offset of the job's host-supplied Gaussians (rng_panels.hpp), -1: device draws
     uint64_t rng0;  // splitmix state0 of the fork that seeds this job
+    uint64_t fork;  // the fork's index in the sketch's RngState (rng.hpp:54-57)
 };
 // job status codes (device int per job)
 enum : int { JOB_ACTIVE = 0, JOB_ZERO = 1, JOB_DEAD = 2 };
 
 // init: X columns <- first r Gaussians of the job's fork (gate: normalized;
 // simul: Pi row-major r x k), zero below r; status from trace(G[0:r,0:r]).
+// panel (nullable): host-supplied Gaussians, job j's at panel + jobs[j].panel
 void iter_init(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg,
-               double* X, int ldx, int R, int* status);
+               double* X, int ldx, int R, int* status, const double* panel = nullptr);
 // normalization after product phase `phase` (Y = G X already computed):
 //  gate : phase < nphase-1 -> X <- Y / ||Y|| (1e-300 check); last -> s1sq = X.Y
 //  simul: S = X^T Y, T = S^{-1/2} (eig, clamped), [last: H = X T], X <- Y T,

@@ -88,6 +88,8 @@ Sketch::Sketch(const aero_cfg& cfg) {
     mode_ = cfg.theta_mode;
     exact_ = (cfg.flags & AERO_FLAG_EXACT) != 0;
     profiling = (cfg.flags & AERO_FLAG_PROFILE) != 0;
+    host_rng_default_ = (cfg.flags & AERO_FLAG_HOST_RNG) != 0;
+    if (host_rng_default_) rng_.set_host();
     dev_ = cfg.device;
     cap_ = 2 * ell_;
     kp_ = power_iter_count(d_);
@@ -101,7 +103,9 @@ Sketch::Sketch(const aero_cfg& cfg) {
     G_.alloc((size_t)cap_ * cap_);
     fill_zero(st_, G_.p, (int64_t)cap_ * cap_);
     ldx_ = cap_;
-    ncols_ = std::max(3 * max_batch_, 64);
+    // job columns: a batch's 3 per row, or one simul_iter at the largest
+    // doubling rank kmax = min(ell, d) (sketch.cpp:112-138)
+    ncols_ = std::max({3 * max_batch_, 64, std::min(ell_, d_)});
     X_.alloc((size_t)ldx_ * ncols_);
     Y_.alloc((size_t)ldx_ * ncols_);
     H_.alloc((size_t)ldx_ * ncols_);
@@ -180,6 +184,12 @@ uint64_t Sketch::fork_state0(uint64_t n) const {
 }
 
 void Sketch::synchronize() { AERO_CUDA(cudaStreamSynchronize(st_)); }
+
+void Sketch::set_rng_source(bool host, aero_rng_fill fn, void* ctx) {
+    if (fn) rng_.set_callback(fn, ctx);
+    else if (host) rng_.set_host();
+    else rng_.set_device();
+}
 
 // ---------------------------------------------------------------- arena
 Chunk* Sketch::arena_alloc(int xi, int* col) {
@@ -264,6 +274,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         maxphase = std::max(maxphase, jobs_h_[j].nphase);
         ncol_total = std::max(ncol_total, jobs_h_[j].col + jobs_h_[j].k);
     }
+    prepare_rng(njobs);
     AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob) * njobs, cudaMemcpyHostToDevice, st_));
     AERO_CUDA(cudaMemcpyAsync(colmask_d_, colmask_h_, sizeof(int) * ncol_total,
                               cudaMemcpyHostToDevice, st_));
@@ -277,7 +288,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         double flops = 0.0;
         for (int j = 0; j < njobs; ++j) flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k * jobs_h_[j].nphase;
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
-        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_, panel_d_);
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
         iterate_warp(st_, jobs_d_, njobs, G_.p, cap_, R, X_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p, kv_, clamp_d_,
                      max_k);
@@ -306,7 +317,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         oz_.reserve_x(phase_h_[0]);
         AERO_CUDA(cudaMemcpyAsync(phase_d_, phase_h_, sizeof(int) * 2 * kMaxPhases, cudaMemcpyHostToDevice, st_));
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
-        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_, panel_d_);
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
         static int sms = 0;
         if (!sms) AERO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_));
@@ -347,7 +358,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         }
         AERO_CUDA(cudaMemcpyAsync(phase_d_, phase_h_, sizeof(int) * 2 * kMaxPhases, cudaMemcpyHostToDevice, st_));
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
-        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+        iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_, panel_d_);
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
         iterate_persistent(st_, jobs_d_, njobs, maxphase, R, G_.p, cap_, X_.p, ldx_, H_.p, status_d_, sig_.p,
                            vr_.p, kv_, clamp_d_, ws_.p, phase_d_, phase_d_ + kMaxPhases, bar_d_, max_k, grid);
@@ -359,7 +370,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
         maxphase = 1;  // one timed region below
     } else {
     if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
-    iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_);
+    iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_, panel_d_);
     // large buffers: G sliced once for all phases, products on the int8 tensor cores
     const bool i8 = i8_ && R >= i8_min_rows_;
     if (i8) oz_.prepare(st_, R, G_.p, cap_);
@@ -421,7 +432,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
 
 // simul_iter with k > 64 columns: same r-space iteration, host-driven phases
 // with device GEMMs and the general eigensolver for the k x k Grams.
-void Sketch::run_simul_large(int k, uint64_t rng0, int r) {
+void Sketch::run_simul_large(int k, uint64_t fork, int r) {
     const size_t kk = (size_t)k * k;
     qw_.alloc(3 * kk + 3 * (size_t)k);
     double* S = qw_.p;
@@ -429,12 +440,13 @@ void Sketch::run_simul_large(int k, uint64_t rng0, int r) {
     double* lam = Tm + kk;
     double* sc = lam + k;
     if (vr_.n < kk) vr_.alloc(kk);
-    jobs_h_[0] = IterJob{1, r, k, 0, q_ + 1, 0, rng0};
-    for (int c = 0; c < k; ++c) colmask_h_[c] = r;
     if (k > ncols_) throw InvalidInput("simul_iter: k exceeds work capacity");
+    jobs_h_[0] = IterJob{1, r, k, 0, q_ + 1, -1, fork_state0(fork), fork};
+    for (int c = 0; c < k; ++c) colmask_h_[c] = r;
+    prepare_rng(1);
     AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob), cudaMemcpyHostToDevice, st_));
     AERO_CUDA(cudaMemcpyAsync(colmask_d_, colmask_h_, sizeof(int) * k, cudaMemcpyHostToDevice, st_));
-    iter_init(st_, jobs_d_, 1, G_.p, cap_, X_.p, ldx_, r, status_d_);
+    iter_init(st_, jobs_d_, 1, G_.p, cap_, X_.p, ldx_, r, status_d_, panel_d_);
     AERO_CUDA(cudaMemcpyAsync(status_h_, status_d_, sizeof(int), cudaMemcpyDeviceToHost, st_));
     AERO_CUDA(cudaStreamSynchronize(st_));
     if (status_h_[0] != JOB_ACTIVE) {
@@ -513,12 +525,12 @@ void Sketch::doubling(int k, int64_t t, double theta, aero_event* ev) {
         const uint64_t f = ++forks_;
         bool zero = false;
         if (k <= 64) {
-            jobs_h_[0] = IterJob{1, r_, k, 0, q_ + 1, 0, fork_state0(f)};
+            jobs_h_[0] = IterJob{1, r_, k, 0, q_ + 1, -1, fork_state0(f), f};
             for (int c = 0; c < k; ++c) colmask_h_[c] = r_;
             run_iterate(1, r_, k);
             zero = status_h_[0] == JOB_ZERO;
         } else {
-            run_simul_large(k, fork_state0(f), r_);
+            run_simul_large(k, f, r_);
             zero = status_h_[0] != JOB_ACTIVE;
         }
         const double tail = sig_h_[k - 1] * sig_h_[k - 1];
@@ -551,7 +563,7 @@ void Sketch::single_row(const double* dev_row, int64_t t, double theta, aero_eve
         ev->reduced = 1;
     }
     const uint64_t f = ++forks_;
-    jobs_h_[0] = IterJob{0, r_, 1, 0, kp_ + 1, 0, fork_state0(f)};
+    jobs_h_[0] = IterJob{0, r_, 1, 0, kp_ + 1, -1, fork_state0(f), f};
     colmask_h_[0] = r_;
     run_iterate(1, r_, 1);
     const double s1 = (status_h_[0] == JOB_ACTIVE) ? sig_h_[0] : 0.0;
@@ -586,7 +598,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
         for (int j = 0; j < B; ++j) {
             const int rj = r0 + j + 1;
             const int kj = std::min(2, std::min({ell_, d_, rj}));
-            jobs_h_[njobs++] = IterJob{1, rj, kj, 2 * j, q_ + 1, 0, fork_state0(F + 2 * j + 2)};
+            jobs_h_[njobs++] = IterJob{1, rj, kj, 2 * j, q_ + 1, -1, fork_state0(F + 2 * j + 2), F + 2 * j + 2};
             colmask_h_[2 * j] = rj;
             colmask_h_[2 * j + 1] = (kj == 2) ? rj : 0;
         }
@@ -594,7 +606,7 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
     for (int j = 0; j < B; ++j) {
         const int rj = r0 + j + 1;
         const uint64_t gf = (pat == FIRE1) ? F + 2 * j + 1 : F + j + 1;
-        jobs_h_[njobs++] = IterJob{0, rj, 1, gate_base + j, kp_ + 1, 0, fork_state0(gf)};
+        jobs_h_[njobs++] = IterJob{0, rj, 1, gate_base + j, kp_ + 1, -1, fork_state0(gf), gf};
         colmask_h_[gate_base + j] = rj;
     }
     run_iterate(njobs, R, 2);
@@ -769,6 +781,11 @@ void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld
         for (int64_t j = 0; j < cnt; ++j) {
             if (bad_h_[j]) { good = j; err = "AeroState: non-finite row"; break; }
             if (t[off + j] <= prev) { good = j; err = "AeroState: timestamp regression"; break; }
+            if (mode_ != AERO_THETA_ATTP && theta_per_row && theta_per_row[off + j] < 0.0) {
+                good = j;  // set_theta throws before this row's update (sketch.cpp:33-36)
+                err = "AeroState: theta must be >= 0";
+                break;
+            }
             prev = t[off + j];
         }
         th.resize(good);
@@ -777,7 +794,6 @@ void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld
                 fro_mass_ += nrm_h_[j];
                 th[j] = eps_ * fro_mass_;
             } else if (theta_per_row) {
-                if (theta_per_row[off + j] < 0.0) throw InvalidInput("AeroState: theta must be >= 0");
                 th[j] = theta_per_row[off + j];
             } else {
                 th[j] = theta_;

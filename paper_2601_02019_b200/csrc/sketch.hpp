@@ -14,6 +14,7 @@
 
 #include "../../include/aero_b200.h"
 #include "kernels.cuh"
+#include "rng_panels.hpp"
 
 namespace aero_b200 {
 
@@ -61,6 +62,11 @@ class Sketch {
     void info(aero_info* out) const;
     const aero_event& last_event() const { return last_ev_; }
     void synchronize();
+    // start-vector / Pi panels from the host (rng_panels.hpp): fn == nullptr
+    // with host == true uses the library's host restatement of rng.hpp
+    void set_rng_source(bool host, aero_rng_fill fn, void* ctx);
+    RngPanels::Mode rng_mode() const { return rng_.mode(); }
+    bool host_rng_default() const { return host_rng_default_; }
 
     int d() const { return d_; }
     int ell() const { return ell_; }
@@ -99,7 +105,7 @@ class Sketch {
     void dump_from_job(int col, int k, int xi, int64_t t, double theta, bool zero_buffer);
     // run jobs already written to jobs_h_ (njobs); results in sig_h_/status_h_/clamp_h_
     void run_iterate(int njobs, int R, int max_k);
-    void run_simul_large(int k, uint64_t rng0, int r);
+    void run_simul_large(int k, uint64_t fork, int r);
     uint64_t fork_state0(uint64_t n) const;
     Chunk* arena_alloc(int xi, int* col);
     void arena_release(const SnapRec& s);
@@ -141,6 +147,11 @@ class Sketch {
     // n = 128..192 it beats DMMA); AERO_I8_MIN_ROWS overrides (tests force it on)
     int i8_min_rows_ = getenv("AERO_I8_MIN_ROWS") ? atoi(getenv("AERO_I8_MIN_ROWS")) : 1024;
     OzakiGram oz_;
+    RngPanels rng_;
+    bool host_rng_default_ = false;  // AERO_FLAG_HOST_RNG
+    const double* panel_d_ = nullptr;  // this launch's host-supplied panels (or nullptr)
+    // assign panels to jobs_h_[0..njobs) and upload them (before the jobs H2D)
+    void prepare_rng(int njobs) { panel_d_ = rng_.prepare(st_, jobs_h_, njobs); }
     double host_wall_s_ = 0.0, host_sync_s_ = 0.0;  // dev instrumentation (AERO_HOST_PROF)
     int64_t host_syncs_ = 0;
     int* status_d_ = nullptr;

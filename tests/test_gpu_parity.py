@@ -583,3 +583,94 @@ def test_c2_scale_default_path_properties(orc):
     g = orc.OracleGram(d)
     g.add_block(rows, ts)
     assert g.error(b) <= eps
+
+
+# ---------------------------------------------------------------- host-owned projections
+def test_host_rng_panels_feed_the_engine(orc):
+    """SURVEY.md 8(b) aero_rng_fill / AERO_FLAG_HOST_RNG: the projections the
+    device consumes come from the host -- a caller callback returning the
+    oracle's RngState draws (pinned to the reference's rng.hpp by the golden
+    vectors), or the library's own host restatement, which is bit-identical
+    (tests/test_host_rng.py). Both runs therefore consume the same bits: their
+    sigma estimates agree exactly, and every fork the reference consumed was
+    requested through the FFI with at least the reference's draw count."""
+    d, eps, n = 256, 1 / 16, 600
+    rows = orc.gen_rows(d, 16, 0.9, 0.1, 64.0, 1, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, eps, 1, 1000)
+    ev_ref = ref.update_block(rows, ts)
+    calls = {}
+
+    def fill(fork, count):
+        calls[fork] = max(calls.get(fork, 0), count)
+        return orc.rng_draw(1, 1000, fork, count)
+
+    a = prod.AttpState(d, eps, seed=1, stream=1000)
+    a.set_rng_fill(fill)
+    ev_a = a.update_block(rows, ts)
+    b = prod.AttpState(d, eps, seed=1, stream=1000, host_rng=True)
+    ev_b = b.update_block(rows, ts)
+    assert_trace_equal(ev_a, ev_ref)
+    assert_trace_equal(ev_b, ev_ref)
+    for f in ("sigma1_sq", "tail_sq"):
+        assert np.array_equal(ev_a[f], ev_b[f]), f
+    consumed = set(range(1, int(ev_ref["forks_after"][-1]) + 1))
+    assert consumed <= set(calls), sorted(consumed - set(calls))[:5]
+    # a gate fork needs r draws (linalg.cpp:106-108), a simul_iter fork r*k (linalg.cpp:141)
+    for e in ev_ref[:50]:
+        assert calls[int(e["forks_before"]) + 1] >= e["rows_after"]
+    assert rel_fro(a.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-9
+    assert np.array_equal(a.query_gram(0, n), b.query_gram(0, n))
+    # a failing source surfaces as InvalidInput from the update
+    c = prod.AttpState(d, eps, seed=1, stream=1000)
+    c.set_rng_fill(lambda fork, count: np.zeros(count + 1))
+    with pytest.raises(prod.InvalidInput):
+        c.update_block(rows[:10], ts[:10])
+
+
+# ---------------------------------------------------------------- C2 at BASELINE size vs the oracle
+def _c2_fixture():
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "c2_prefix.npz")
+    if not os.path.exists(p):
+        pytest.skip("tests/golden/c2_prefix.npz missing (tools/make_c2_fixture.py)")
+    return np.load(p)
+
+
+@pytest.mark.parametrize("host_rng", [False, True])
+def test_c2_default_path_matches_oracle_fixture(orc, host_rng):
+    """BASELINE config C2 (d=4096, eps=1/512, ell=1024) on the DEFAULT engine
+    path (speculative batches, persistent int8 tcgen05 iterate once the buffer
+    holds >= 1024 rows, grid eigensolver reduces at rows 2048 and 3073) against
+    the oracle's run over the same 4096 rows (tests/golden/c2_prefix.npz,
+    tools/make_c2_fixture.py): decision trace bit-exact, sigma estimates
+    rel <= 1e-8, the restored Gram probed at five checkpoints rel <= 1e-9
+    (Frobenius) / 1e-9 (probe columns), covariance error within 1e-6 of the
+    oracle's and <= eps."""
+    fx = _c2_fixture()
+    d, eps = 4096, 1 / 512
+    n = int(fx["n"])
+    rows = orc.gen_rows(d, 256, 0.99, 0.05, 256.0, 1, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    w = orc.rng_draw(99, 0, 0, d * 4).reshape(d, 4)
+    s = prod.AttpState(d, eps, seed=1, stream=1000, host_rng=host_rng)
+    pos, evs = 0, []
+    for i, cp in enumerate(fx["probe_t"]):
+        cp = int(cp)
+        evs.append(s.update_block(rows[pos:cp], ts[pos:cp]))
+        pos = cp
+        g = s.query_gram(0, cp)
+        assert abs(np.linalg.norm(g) - fx["gram_fro"][i]) <= 1e-9 * fx["gram_fro"][i], cp
+        pr = g @ w
+        assert np.linalg.norm(pr - fx["probe"][i]) <= 1e-9 * np.linalg.norm(fx["probe"][i]), cp
+    ev = np.concatenate(evs)
+    assert_trace_equal(ev, fx["events"])
+    assert abs(s.fro_mass - float(fx["mass"])) <= 1e-12 * float(fx["mass"])
+    b = s.query(n)
+    gram = torch.from_numpy(rows).cuda()
+    a_gram = gram.T @ gram
+    bt = torch.from_numpy(b).cuda()
+    diff = a_gram - bt.T @ bt
+    err = float(torch.linalg.eigvalsh(diff).abs().max()) / float((gram * gram).sum())
+    assert abs(err - float(fx["err"])) <= 1e-6, (err, float(fx["err"]))
+    assert err <= eps

@@ -485,3 +485,56 @@ def test_cod_error_budget(orc):  # test_amm.cpp:104-122, acceptance check 8
             a, b = s.query()
             den = math.sqrt(np.sum(xs[lo:i] ** 2) * np.sum(ys[lo:i] ** 2))
             assert orc.spectral_norm(p - a @ b.T) / den <= eps
+
+
+# ---------------------------------------------------------------- amplification (sketch.cpp:45-80)
+def test_amplified_requires_delta(orc):  # test_sketch.cpp:94-97
+    s = orc.AeroState(4, 0.5, 0.0, 0, 0)
+    with pytest.raises(orc.InvalidInput):
+        s.update_amplified(np.ones(4), 1)
+    for bad in (-0.1, 1.0, 2.0):
+        with pytest.raises(orc.InvalidInput):
+            orc.AeroState(4, 0.5, 0.0, 0, 0, delta=bad)
+
+
+def test_amplified_two_candidates_per_doubling_step(orc):  # test_sketch.cpp:99-112
+    s = orc.AeroState(8, 0.5, 2.0, 9, 0, delta=0.01)
+    saw_dump = False
+    for i in range(1, 61):
+        ev = s.update_amplified(gaussian_vec(orc, 8, 200 + i), i)
+        if ev["doubling_steps"] > 0:
+            assert ev["simul_calls"] == 2 * ev["doubling_steps"]  # r = 2 at delta = 0.01
+            # r candidates x (1 simul_iter + s = 10 power iterations) forks per step
+            assert ev["forks_after"] - ev["forks_before"] == 1 + 2 * 11 * ev["doubling_steps"]
+            saw_dump = saw_dump or bool(ev["dumped"])
+    assert saw_dump
+
+
+def test_amplified_acceptance_check_11(orc):  # acceptance.cpp:390-408
+    # amplified window sketch keeps the end-to-end error budget (check_window_end_to_end, :152-187)
+    d, n, t_end, eps = 32, 500, 1500, 0.2
+    for seed in range(3):
+        s = orc.MlState(d, n, 32.0, eps, seed + 100, 1000, delta=0.01)
+        g = orc.OracleGram(d, n, 100000)
+        rows = uniform_rows(orc, t_end, d, seed + 100, 0)
+        for b in range(0, t_end, 20):
+            s.update_block(rows[b:b + 20], np.arange(b + 1, b + 21))
+            g.add_block(rows[b:b + 20], np.arange(b + 1, b + 21))
+            assert g.error(s.query()["sketch"]) <= eps
+    # trace invariant: two factorization candidates per doubling step
+    s = orc.AeroState(32, 0.2, 5.0, 1, 61, delta=0.01)
+    rows = uniform_rows(orc, 300, 32, 1, 62)
+    ev = s.update_block_amplified(rows, np.arange(1, 301))
+    on = ev["doubling_steps"] > 0
+    assert on.any() and np.all(ev["simul_calls"][on] == 2 * ev["doubling_steps"][on])
+
+
+def test_attp_amplified_uses_update_amplified(orc):  # attp.hpp:17-26
+    rows = uniform_rows(orc, 120, 16, 3, 0)
+    a = orc.AttpState(16, 0.25, 3, 1000, delta=0.01)
+    ev = a.update_block(rows, np.arange(1, 121))
+    on = ev["doubling_steps"] > 0
+    assert on.any() and np.all(ev["simul_calls"][on] == 2 * ev["doubling_steps"][on])
+    b = orc.AttpState(16, 0.25, 3, 1000)
+    ev_b = b.update_block(rows, np.arange(1, 121))
+    assert np.all(ev_b["simul_calls"] == ev_b["doubling_steps"])
