@@ -56,6 +56,8 @@ typedef struct aero_cfg {
     int32_t theta_mode; /* AERO_THETA_FIXED or AERO_THETA_ATTP */
     int32_t flags;      /* AERO_FLAG_* */
     int32_t max_batch;  /* speculative batch rows (0 = auto) */
+    double delta;       /* probability amplification bound in (0, 1) (sketch.hpp:44-46); 0 = none.
+                           AttpState with delta amplifies every update (attp.hpp:24) */
 } aero_cfg;
 
 /* per-row event record (UpdateStats, sketch.hpp:33-39, plus the trace the
@@ -106,6 +108,10 @@ int aero_set_rng_fill(aero_sketch* h, aero_rng_fill fn, void* ctx);
  * (nullable) receives one aero_event per row. */
 int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
                       const double* theta_per_row, aero_event* log_out);
+/* n sequential AeroState::update_amplified calls (sketch.cpp:45-48; needs
+ * cfg.delta > 0, else AERO_INVALID_INPUT before any row is absorbed) */
+int aero_update_block_amplified(aero_sketch* h, const double* rows, int64_t n, int64_t ld,
+                                const int64_t* t, const double* theta_per_row, aero_event* log_out);
 /* same, rows already resident in device memory (ld in elements). The rows
  * are read on aero_stream(h): the caller must order their producer before it
  * (cudaStreamWaitEvent on aero_stream(h), or a completed producer stream). */
@@ -161,6 +167,10 @@ typedef struct aero_ml_info {
 } aero_ml_info;
 int aero_ml_create(int32_t d, int64_t window, double r_max, double eps, uint64_t seed,
                    uint64_t stream, int32_t device, aero_ml** out);
+/* MlState(d, n, r_max, eps, rng, delta) with amplified level updates
+ * (sliding_window.cpp:15-30, 90-91) */
+int aero_ml_create_amplified(int32_t d, int64_t window, double r_max, double eps, double delta,
+                             uint64_t seed, uint64_t stream, int32_t device, aero_ml** out);
 int aero_ml_destroy(aero_ml* h);
 int aero_ml_update_block(aero_ml* h, const double* rows, int64_t n, int64_t ld, const int64_t* t);
 int aero_ml_update_block_device(aero_ml* h, const double* rows_device, int64_t n, int64_t ld,

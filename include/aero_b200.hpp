@@ -63,8 +63,9 @@ struct Snapshot {
 class AeroState {
   public:
     // AeroState(d, eps, theta, RngState(seed, stream)) (sketch.cpp:22-31)
+    // delta > 0: probability amplification (sketch.hpp:44-46)
     AeroState(int d, double eps, double theta, std::uint64_t seed, std::uint64_t stream,
-              int device = 0, int theta_mode = AERO_THETA_FIXED) {
+              int device = 0, int theta_mode = AERO_THETA_FIXED, double delta = 0.0) {
         aero_cfg c{};
         c.d = d;
         c.eps = eps;
@@ -73,6 +74,7 @@ class AeroState {
         c.stream = stream;
         c.device = device;
         c.theta_mode = theta_mode;
+        c.delta = delta;
         check(aero_create(&c, &h_));
     }
     AeroState(const AeroState&) = delete;
@@ -85,6 +87,12 @@ class AeroState {
         if ((int)a.size() != d()) throw InvalidInput("AeroState: row dimension mismatch");
         update(a.data(), i);
     }
+    // sketch.cpp:45-48
+    void update_amplified(const double* a, std::int64_t i) {
+        check(aero_update_block_amplified(h_, a, 1, d(), &i, nullptr, nullptr));
+    }
+    // caller-owned random projections (aero_set_rng_fill)
+    void set_rng_fill(aero_rng_fill fn, void* ctx) { check(aero_set_rng_fill(h_, fn, ctx)); }
     // n sequential updates of row-major rows (the block API the reference lacks)
     void update_block(const double* rows, std::int64_t n, const std::int64_t* t,
                       std::vector<UpdateStats>* log = nullptr) {

@@ -53,7 +53,7 @@ _ERRS = {1: InvalidInput, 2: FormatError, 3: ProtocolError, 4: OracleCapExceeded
 class Cfg(C.Structure):
     _fields_ = [("d", i32), ("ell", i32), ("eps", f64), ("theta", f64), ("eps_si", f64),
                 ("seed", u64), ("stream", u64), ("device", i32), ("theta_mode", i32),
-                ("flags", i32), ("max_batch", i32)]
+                ("flags", i32), ("max_batch", i32), ("delta", f64)]
 
 
 class Event(C.Structure):
@@ -111,6 +111,7 @@ SIGNATURES = [
     ("aero_set_rng_fill", i32, [vp, vp, vp]),
     ("aero_update_block", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_update_block_device", i32, [vp, vp, i64, i64, P(i64), P(f64), P(Event)]),
+    ("aero_update_block_amplified", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_query", i32, [vp, i64, i64, P(f64)]),
     ("aero_query_gram", i32, [vp, i64, i64, P(f64)]),
     ("aero_residual", i32, [vp, P(f64), i64]),
@@ -126,6 +127,7 @@ SIGNATURES = [
     ("aero_get_profile", i32, [vp, P(Profile)]),
     ("aero_reset_profile", i32, [vp]),
     ("aero_ml_create", i32, [i32, i64, f64, f64, u64, u64, i32, P(vp)]),
+    ("aero_ml_create_amplified", i32, [i32, i64, f64, f64, f64, u64, u64, i32, P(vp)]),
     ("aero_ml_destroy", i32, [vp]),
     ("aero_ml_update_block", i32, [vp, P(f64), i64, i64, P(i64)]),
     ("aero_ml_update_block_device", i32, [vp, vp, i64, i64, P(i64)]),
@@ -281,7 +283,7 @@ class AeroState:
     a caller-owned source instead."""
 
     def __init__(self, d, eps, theta=0.0, seed=0, stream=0, device=0, ell=0, theta_mode=AERO_THETA_FIXED,
-                 exact=False, max_batch=0, profile=False, host_rng=False, _handle=None, _owner=None):
+                 exact=False, max_batch=0, profile=False, host_rng=False, delta=None, _handle=None, _owner=None):
         self._owner = _owner
         self._rng_cb = None
         if _handle is not None:
@@ -291,7 +293,7 @@ class AeroState:
                       device=device, theta_mode=theta_mode,
                       flags=(AERO_FLAG_EXACT if exact else 0) | (AERO_FLAG_PROFILE if profile else 0)
                       | (AERO_FLAG_HOST_RNG if host_rng else 0),
-                      max_batch=max_batch)
+                      max_batch=max_batch, delta=float(delta or 0.0))
             h = vp()
             _chk(lib().aero_create(C.byref(cfg), C.byref(h)))
             self._h, self._own = h, True
@@ -377,6 +379,22 @@ class AeroState:
     def update(self, a, i):
         return self.update_block(np.asarray(a, np.float64)[None, :], [i])[0]
 
+    def update_block_amplified(self, rows, ts, thetas=None):
+        """n sequential update_amplified calls (sketch.cpp:45-48), host rows."""
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = ts.shape[0]
+        th = _f64(thetas) if thetas is not None else None
+        rows = _f64(rows)
+        if rows.ndim != 2 or rows.shape[1] != self.d:
+            raise InvalidInput("AeroState: row dimension mismatch")
+        _check_block(rows.shape[0], n, th)
+        ev = (Event * max(n, 1))()
+        _chk(lib().aero_update_block_amplified(self._h, _dp(rows), n, self.d, _lp(ts), _dp(th), ev))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy()
+
+    def update_amplified(self, a, i):
+        return self.update_block_amplified(np.asarray(a, np.float64)[None, :], [i])[0]
+
     def query(self, lb, ub):
         out = np.empty((self.ell, self.d))
         _chk(lib().aero_query(self._h, lb, ub, _dp(out)))
@@ -443,9 +461,9 @@ class AttpState(AeroState):
     """reference AttpState (attp.hpp:15-43): theta = eps * running mass."""
 
     def __init__(self, d, eps, seed=0, stream=0, device=0, exact=False, max_batch=0, profile=False,
-                 host_rng=False):
+                 host_rng=False, delta=None):
         super().__init__(d, eps, 0.0, seed, stream, device, theta_mode=AERO_THETA_ATTP,
-                         exact=exact, max_batch=max_batch, profile=profile, host_rng=host_rng)
+                         exact=exact, max_batch=max_batch, profile=profile, host_rng=host_rng, delta=delta)
 
     @property
     def inner(self):
@@ -466,9 +484,10 @@ class AttpState(AeroState):
 class MlState:
     """reference MlState (sliding_window.hpp:39-81)."""
 
-    def __init__(self, d, n, r_max, eps, seed=0, stream=0, device=0):
+    def __init__(self, d, n, r_max, eps, seed=0, stream=0, device=0, delta=None):
         h = vp()
-        _chk(lib().aero_ml_create(d, n, r_max, eps, seed, stream, device, C.byref(h)))
+        _chk(lib().aero_ml_create_amplified(d, n, r_max, eps, float(delta or 0.0), seed, stream, device,
+                                            C.byref(h)))
         self._h, self.d, self.n = h, d, n
         inf = self.info()
         self.levels, self.ell = inf.levels, inf.ell

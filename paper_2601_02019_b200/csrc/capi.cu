@@ -95,6 +95,15 @@ int aero_update_block(aero_sketch* h, const double* rows, int64_t n, int64_t ld,
     }
     return guard([&] { h->s->update_block(rows, false, n, ld, t, theta_per_row, log_out); });
 }
+int aero_update_block_amplified(aero_sketch* h, const double* rows, int64_t n, int64_t ld, const int64_t* t,
+                                const double* theta_per_row, aero_event* log_out) {
+    REQ(h);
+    if (n > 0) {
+        REQ(rows);
+        REQ(t);
+    }
+    return guard([&] { h->s->update_block(rows, false, n, ld, t, theta_per_row, log_out, true); });
+}
 int aero_update_block_device(aero_sketch* h, const double* rows_device, int64_t n, int64_t ld,
                              const int64_t* t, const double* theta_per_row, aero_event* log_out) {
     REQ(h);
@@ -305,13 +314,17 @@ struct aero_ml {
 };
 int aero_ml_create(int32_t d, int64_t window, double r_max, double eps, uint64_t seed,
                    uint64_t stream, int32_t device, aero_ml** out) {
+    return aero_ml_create_amplified(d, window, r_max, eps, 0.0, seed, stream, device, out);
+}
+int aero_ml_create_amplified(int32_t d, int64_t window, double r_max, double eps, double delta,
+                             uint64_t seed, uint64_t stream, int32_t device, aero_ml** out) {
     REQ(out);
     return guard([&] {
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw CudaError("no CUDA device: the AeroSketch B200 path has no CPU fallback");
         auto* h = new aero_ml;
-        h->e = new MlEngine(d, window, r_max, eps, seed, stream, device);
+        h->e = new MlEngine(d, window, r_max, eps, seed, stream, device, delta);
         for (int j = 0; j < h->e->levels(); ++j) h->levels.push_back(aero_sketch{&h->e->level(j), false});
         *out = h;
     });

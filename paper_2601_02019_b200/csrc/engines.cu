@@ -24,8 +24,8 @@ void shrink_device(cudaStream_t st, int d, int ell, double* B, double* w, double
 // ============================================================================
 // sliding_window.cpp:15-30
 MlEngine::MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, uint64_t stream,
-                   int device)
-    : d_(d), dev_(device), n_(n), r_max_(r_max), eps_(eps) {
+                   int device, double delta)
+    : d_(d), dev_(device), n_(n), r_max_(r_max), eps_(eps), amplified_(delta != 0.0) {
     if (n < 1) throw InvalidInput("MlState: window size must be >= 1");
     if (r_max < 1.0) throw InvalidInput("MlState: r_max must be >= 1 (squared norms in [1, R])");
     if (!(eps > 0.0 && eps <= 1.0)) throw InvalidInput("MlState: eps out of (0,1]");
@@ -44,6 +44,7 @@ MlEngine::MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, ui
         c.stream = fork_stream(stream, (uint64_t)(j + 1));  // levels_[j] gets rng.fork()
         c.device = device;
         c.theta_mode = AERO_THETA_FIXED;
+        c.delta = delta;
         levels_.emplace_back(new Sketch(c));
         heavy_.emplace_back();
         lq_.emplace_back();
@@ -145,7 +146,7 @@ void MlEngine::update_block(const double* rows, bool device, int64_t n, int64_t 
                         src = gath[lv].p;
                     }
                     levels_[lv]->update_block(src, true, (int64_t)idx.size(), d_, ts.data(), nullptr,
-                                              nullptr);
+                                              nullptr, amplified_);
                     levels_[lv]->synchronize();
                 } catch (...) {
                     errs[lv] = std::current_exception();

@@ -19,7 +19,8 @@ struct HeavyRow {
 };
 class MlEngine {
   public:
-    MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, uint64_t stream, int device);
+    MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, uint64_t stream, int device,
+             double delta = 0.0);
     void update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t);
     void query(double* out_host, aero_ml_query_result* res);
     void info(aero_ml_info* out) const;
@@ -40,6 +41,7 @@ class MlEngine {
     int d_, ell_, dev_;
     int64_t n_, cap_, clock_ = 0, norm_warnings_ = 0;
     double r_max_, eps_, window_mass_ = 0.0;
+    bool amplified_ = false;  // levels update_amplified (sliding_window.cpp:90-91)
     std::vector<std::unique_ptr<Sketch>> levels_;
     std::vector<std::deque<HeavyRow>> heavy_;
     std::vector<LevelQueue> lq_;

@@ -81,6 +81,9 @@ Sketch::Sketch(const aero_cfg& cfg) {
     eps_ = cfg.eps;
     ell_ = cfg.ell > 0 ? cfg.ell : static_cast<int>(std::ceil(2.0 / cfg.eps));  // sketch.cpp:30
     eps_si_ = cfg.eps_si > 0.0 ? cfg.eps_si : 0.4;                              // sketch.cpp:23
+    if (cfg.delta != 0.0 && !(cfg.delta > 0.0 && cfg.delta < 1.0))
+        throw InvalidInput("AeroState: delta out of (0, 1)");  // sketch.cpp:28-29
+    delta_ = cfg.delta;
     if (!(eps_si_ > 0.0 && eps_si_ < 1.0)) throw InvalidInput("AeroState: eps_si out of (0,1)");
     theta_ = cfg.theta;
     seed_ = cfg.seed;
@@ -432,7 +435,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
 
 // simul_iter with k > 64 columns: same r-space iteration, host-driven phases
 // with device GEMMs and the general eigensolver for the k x k Grams.
-void Sketch::run_simul_large(int k, uint64_t fork, int r) {
+void Sketch::run_simul_large(int k, uint64_t fork, int r, int q) {
     const size_t kk = (size_t)k * k;
     qw_.alloc(3 * kk + 3 * (size_t)k);
     double* S = qw_.p;
@@ -441,7 +444,7 @@ void Sketch::run_simul_large(int k, uint64_t fork, int r) {
     double* sc = lam + k;
     if (vr_.n < kk) vr_.alloc(kk);
     if (k > ncols_) throw InvalidInput("simul_iter: k exceeds work capacity");
-    jobs_h_[0] = IterJob{1, r, k, 0, q_ + 1, -1, fork_state0(fork), fork};
+    jobs_h_[0] = IterJob{1, r, k, 0, q + 1, -1, fork_state0(fork), fork};
     for (int c = 0; c < k; ++c) colmask_h_[c] = r;
     prepare_rng(1);
     AERO_CUDA(cudaMemcpyAsync(jobs_d_, jobs_h_, sizeof(IterJob), cudaMemcpyHostToDevice, st_));
@@ -453,14 +456,14 @@ void Sketch::run_simul_large(int k, uint64_t fork, int r) {
         for (int a = 0; a < k; ++a) sig_h_[a] = 0.0;
         return;
     }
-    for (int p = 0; p <= q_; ++p) {
+    for (int p = 0; p <= q; ++p) {
         gemm_product(st_, r, k, r, G_.p, cap_, X_.p, ldx_, Y_.p, ldx_, colmask_d_, ws_.p, ws_.n);
         dgemm(st_, true, false, k, k, r, 1.0, X_.p, ldx_, Y_.p, ldx_, 0.0, S, k);
         eigh(st_, k, S, k, lam);
         k_inv_sqrt_clamp<<<1, 1, 0, st_>>>(lam, k, sc);
         AERO_LAUNCHED();
         scale_columns(st_, k, k, S, k, sc);  // T = W diag(lam^-1/2)
-        if (p == q_) dgemm(st_, false, false, r, k, k, 1.0, X_.p, ldx_, S, k, 0.0, H_.p, ldx_);
+        if (p == q) dgemm(st_, false, false, r, k, k, 1.0, X_.p, ldx_, S, k, 0.0, H_.p, ldx_);
         dgemm(st_, false, false, r, k, k, 1.0, Y_.p, ldx_, S, k, 0.0, X_.p, ldx_);
     }
     dgemm(st_, true, false, k, k, r, 1.0, X_.p, ldx_, X_.p, ldx_, 0.0, vr_.p, k);
@@ -514,6 +517,100 @@ void Sketch::dump_from_job(int col, int k, int xi, int64_t t, double theta, bool
     snaps_.push_back(s);
 }
 
+// ---------------------------------------------------------------- amplification
+// sketch.cpp:55-79 in Gram (r-space) form. Candidate h: simul_iter at eps_si =
+// 0.2 gives H (r x k), V (k x k), sigma; z = C'^T (H V). Its residual
+// at_res = C'^T - z z^T C'^T has Gram  G_res = at_res^T at_res
+// = G - 2 P P^T + P (z^T z) P^T  with P = C' z = G (H V) and z^T z = (HV)^T P
+// (the dump's downdate formula). s power_iteration gates on G_res (forks
+// after the candidate's) score it by their max; the smallest score wins.
+bool Sketch::amplified_factorize(int k, aero_event* ev) {
+    const double delta = delta_;
+    const int rc = static_cast<int>(std::ceil(std::log(2.0 / delta) / std::log(100.0)));
+    const int q02 = simul_q(d_, 0.2);
+    auto run_candidate = [&](uint64_t f) -> bool {  // -> buffer exactly zero
+        ev->simul_calls++;
+        if (k <= 64) {
+            jobs_h_[0] = IterJob{1, r_, k, 0, q02 + 1, -1, fork_state0(f), f};
+            for (int c = 0; c < k; ++c) colmask_h_[c] = r_;
+            run_iterate(1, r_, k);
+            return status_h_[0] == JOB_ZERO;
+        }
+        run_simul_large(k, f, r_, q02);
+        return status_h_[0] != JOB_ACTIVE;
+    };
+    if (rc <= 1) return run_candidate(++forks_);  // sketch.cpp:57-60
+    const int s = static_cast<int>(std::ceil(2.0 * std::log(2.0 / delta) / std::log(3.0)));
+    if (s > ncols_) throw InvalidInput("amplification: s exceeds work capacity");
+    const int r = r_, rl = r + (r & 1);
+    const size_t kk = (size_t)k * k;
+    Gres_.alloc((size_t)cap_ * cap_);
+    Hc_.alloc((size_t)rl * k);
+    Hb_.alloc((size_t)rl * k);
+    vrc_.alloc(kk);
+    vrb_.alloc(kk);
+    qy_.alloc((size_t)rl * k * 2 + kk + 64);
+    double* HV = qy_.p;
+    double* P = HV + (size_t)rl * k;
+    double* ZZ = P + (size_t)rl * k;
+    std::vector<double> best_sig(k), cur_sig(k);
+    double best_cost = 0.0;
+    bool best_zero = false;
+    for (int h = 0; h < rc; ++h) {
+        const bool zero = run_candidate(++forks_);
+        const double* vr = vr_.p;  // the candidate is job 0 (col 0, k x k at vr_)
+        for (int a = 0; a < k; ++a) cur_sig[a] = sig_h_[a];
+        // keep the candidate's factors before the scoring gates overwrite H / vr
+        AERO_CUDA(cudaMemcpy2DAsync(Hc_.p, sizeof(double) * rl, H_.p, sizeof(double) * ldx_, sizeof(double) * r, k,
+                                    cudaMemcpyDeviceToDevice, st_));
+        AERO_CUDA(cudaMemcpyAsync(vrc_.p, vr, sizeof(double) * kk, cudaMemcpyDeviceToDevice, st_));
+        // residual Gram of this candidate (z = I for an all-zero buffer: G_res = 0)
+        if (zero) {
+            fill_zero(st_, Gres_.p, (int64_t)cap_ * cap_);
+        } else {
+            copy_matrix(st_, r, r, G_.p, cap_, Gres_.p, cap_);
+            dgemm(st_, false, false, r, k, k, 1.0, Hc_.p, rl, vrc_.p, k, 0.0, HV, rl);  // H V
+            dgemm(st_, false, false, r, k, r, 1.0, G_.p, cap_, HV, rl, 0.0, P, rl);      // P = G H V
+            dgemm(st_, true, false, k, k, r, 1.0, HV, rl, P, rl, 0.0, ZZ, k);           // z^T z
+            add_identity(st_, k, ZZ, k, -2.0);
+            dgemm(st_, false, false, r, k, k, 1.0, P, rl, ZZ, k, 0.0, HV, rl);          // P (z^T z - 2I)
+            dgemm(st_, false, true, r, r, k, 1.0, HV, rl, P, rl, 1.0, Gres_.p, cap_);
+            symmetrize(st_, r, Gres_.p, cap_);
+        }
+        // s power iterations on the residual (sketch.cpp:67-69), one batched launch
+        const uint64_t f0 = forks_;
+        for (int i = 0; i < s; ++i) {
+            jobs_h_[i] = IterJob{0, r, 1, i, kp_ + 1, -1, fork_state0(f0 + 1 + i), f0 + 1 + i};
+            colmask_h_[i] = r;
+        }
+        forks_ += s;
+        std::swap(G_.p, Gres_.p);
+        try {
+            run_iterate(s, r, 1);
+        } catch (...) {
+            std::swap(G_.p, Gres_.p);
+            throw;
+        }
+        std::swap(G_.p, Gres_.p);
+        double cost = 0.0;
+        for (int i = 0; i < s; ++i) cost = std::max(cost, status_h_[i] == JOB_ACTIVE ? sig_h_[i] : 0.0);
+        if (h == 0 || cost < best_cost) {
+            best_cost = cost;
+            best_zero = zero;
+            best_sig = cur_sig;
+            std::swap(Hb_.p, Hc_.p);
+            std::swap(vrb_.p, vrc_.p);
+        }
+    }
+    // the winner back where dump_from_job reads a job-0 factorization
+    AERO_CUDA(cudaMemcpy2DAsync(H_.p, sizeof(double) * ldx_, Hb_.p, sizeof(double) * rl, sizeof(double) * r, k,
+                                cudaMemcpyDeviceToDevice, st_));
+    AERO_CUDA(cudaMemcpyAsync(vr_.p, vrb_.p, sizeof(double) * kk, cudaMemcpyDeviceToDevice, st_));
+    for (int a = 0; a < k; ++a) sig_h_[a] = best_sig[a];
+    status_h_[0] = best_zero ? JOB_ZERO : JOB_ACTIVE;
+    return best_zero;
+}
+
 // ---------------------------------------------------------------- doubling
 // sketch.cpp:108-139 for one row, starting at rank k (forks consumed so far
 // are already in forks_)
@@ -521,16 +618,20 @@ void Sketch::doubling(int k, int64_t t, double theta, aero_event* ev) {
     const int kmax = std::min({ell_, d_, r_});
     while (true) {
         ev->doubling_steps++;
-        ev->simul_calls++;
-        const uint64_t f = ++forks_;
         bool zero = false;
-        if (k <= 64) {
+        if (amp_) {
+            zero = amplified_factorize(k, ev);
+        } else if (k <= 64) {
+            ev->simul_calls++;
+            const uint64_t f = ++forks_;
             jobs_h_[0] = IterJob{1, r_, k, 0, q_ + 1, -1, fork_state0(f), f};
             for (int c = 0; c < k; ++c) colmask_h_[c] = r_;
             run_iterate(1, r_, k);
             zero = status_h_[0] == JOB_ZERO;
         } else {
-            run_simul_large(k, f, r_);
+            ev->simul_calls++;
+            const uint64_t f = ++forks_;
+            run_simul_large(k, f, r_, q_);
             zero = status_h_[0] != JOB_ACTIVE;
         }
         const double tail = sig_h_[k - 1] * sig_h_[k - 1];
@@ -589,7 +690,8 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
     const uint64_t F = forks_;
     // predict the majority outcome of recent rows (a lone non-firing row in a
     // firing regime ends one batch, not two)
-    const Pattern pat = (fire_ema_ >= 0.5) ? FIRE1 : NOFIRE;
+    // (amplified rows finish every fired gate exactly: r candidates + scoring)
+    const Pattern pat = (!amp_ && fire_ema_ >= 0.5) ? FIRE1 : NOFIRE;
     append_rows(dev_rows, B);
     const int R = r0 + (int)B;
     int njobs = 0;
@@ -751,9 +853,12 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
 
 // ---------------------------------------------------------------- update
 void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t,
-                          const double* theta_per_row, aero_event* log) {
+                          const double* theta_per_row, aero_event* log, bool amplified) {
     if (n <= 0) return;
     if (ld < d_) throw InvalidInput("AeroState: row dimension mismatch");
+    if (amplified && delta_ == 0.0)  // sketch.cpp:46
+        throw InvalidInput("AeroState: amplification requested without delta");
+    amp_ = amplified || (mode_ == AERO_THETA_ATTP && delta_ > 0.0);  // attp.hpp:24
     AERO_CUDA(cudaSetDevice(dev_));
     std::vector<aero_event> local;
     if (!log) {

@@ -48,8 +48,11 @@ class Sketch {
 
     void set_theta(double th);
     // rows: host or device pointer (row-major, ld); n sequential updates
+    // amplified: n sequential update_amplified calls (sketch.cpp:45-48); an
+    // AttpState built with delta always amplifies (attp.hpp:24)
     void update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t,
-                      const double* theta_per_row, aero_event* log);
+                      const double* theta_per_row, aero_event* log, bool amplified = false);
+    double delta() const { return delta_; }
     // restored Gram (sketch.cpp:146-159) into device d x d buffer; returns ptr
     const double* query_gram_device(int64_t lb, int64_t ub);
     void query(int64_t lb, int64_t ub, double* out_host);       // ell x d
@@ -105,7 +108,11 @@ class Sketch {
     void dump_from_job(int col, int k, int xi, int64_t t, double theta, bool zero_buffer);
     // run jobs already written to jobs_h_ (njobs); results in sig_h_/status_h_/clamp_h_
     void run_iterate(int njobs, int R, int max_k);
-    void run_simul_large(int k, uint64_t fork, int r);
+    void run_simul_large(int k, uint64_t fork, int r, int q);
+    // sketch.cpp:55-79: r candidates at eps_si = 0.2 scored by s power
+    // iterations on the residual; leaves the winner in H col 0 / vr / sig_h_
+    // and returns whether its buffer was exactly zero
+    bool amplified_factorize(int k, aero_event* ev);
     uint64_t fork_state0(uint64_t n) const;
     Chunk* arena_alloc(int xi, int* col);
     void arena_release(const SnapRec& s);
@@ -118,6 +125,9 @@ class Sketch {
     cudaEvent_t evA_ = nullptr, evB_ = nullptr;
     cudaEvent_t ev_at(size_t i);
     double eps_, eps_si_;
+    double delta_ = 0.0;  // amplification failure bound (sketch.hpp:44-46), 0 = none
+    bool amp_ = false;    // the current update_block call is amplified
+    DeviceBuf Gres_, Hc_, Hb_, vrc_, vrb_;  // amplification: residual Gram, candidate / best factors
     uint64_t seed_, stream_;
     int dev_;
     cudaStream_t st_ = nullptr;

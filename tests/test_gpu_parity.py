@@ -674,3 +674,66 @@ def test_c2_default_path_matches_oracle_fixture(orc, host_rng):
     err = float(torch.linalg.eigvalsh(diff).abs().max()) / float((gram * gram).sum())
     assert abs(err - float(fx["err"])) <= 1e-6, (err, float(fx["err"]))
     assert err <= eps
+
+
+# ---------------------------------------------------------------- update_amplified (sketch.cpp:45-80)
+def test_amplified_updates_match_oracle(orc):
+    """AeroState::update_amplified: r = 2 candidates at eps_si = 0.2, each
+    scored by s = 10 power iterations on its residual, the smaller score
+    kept (test_sketch.cpp:99-112 shape). Trace bit-exact (incl. forks: 1 +
+    2*11 per doubling step), snapshots and Gram against the oracle; without
+    delta the call is rejected before any row is absorbed."""
+    rows = np.stack([gaussian_vec(orc, 8, 200 + i) for i in range(1, 61)])
+    ts = np.arange(1, 61)
+    ref = orc.AeroState(8, 0.5, 2.0, 9, 0, delta=0.01)
+    ev_ref = ref.update_block_amplified(rows, ts)
+    s = prod.AeroState(8, 0.5, 2.0, seed=9, stream=0, delta=0.01)
+    ev = s.update_block_amplified(rows, ts)
+    assert_trace_equal(ev, ev_ref)
+    on = ev["doubling_steps"] > 0
+    assert on.any() and ev["dumped"].any()
+    assert np.all(ev["simul_calls"][on] == 2 * ev["doubling_steps"][on])
+    assert rel_fro(s.query_gram(0, 60), ref.query_gram(0, 60)) < 1e-9
+    plain = prod.AeroState(4, 0.5, 0.0)
+    with pytest.raises(prod.InvalidInput):
+        plain.update_amplified(np.ones(4), 1)
+    assert plain.clock == 0
+
+
+def test_amplified_attp_stream_matches_oracle(orc):
+    """AttpState with delta amplifies every update (attp.hpp:24) -- on a
+    stream of the C1 generator at d=256 (buffers > 64 rows: the batched
+    gates and the GPU residual-Gram scoring at real sizes)."""
+    d, eps, n = 256, 1 / 16, 500
+    rows = orc.gen_rows(d, 16, 0.9, 0.1, 64.0, 1, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, eps, 1, 1000, delta=0.01)
+    ev_ref = ref.update_block(rows, ts)
+    s = prod.AttpState(d, eps, seed=1, stream=1000, delta=0.01)
+    ev = s.update_block(rows, ts)
+    assert_trace_equal(ev, ev_ref)
+    assert ev["dumped"].sum() >= 1 and ev["reduced"].sum() >= 1
+    assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-9
+
+
+def test_amplified_window_bookkeeping(orc):
+    """MlState with delta (sliding_window.cpp:90-91), acceptance check 11
+    shape: queues, heavy rows and query level bit-exact, error <= eps."""
+    d, n_win, eps, T = 32, 500, 0.2, 600
+    ref = orc.MlState(d, n_win, 32.0, eps, 100, 1000, delta=0.01)
+    s = prod.MlState(d, n_win, 32.0, eps, seed=100, stream=1000, delta=0.01)
+    g = orc.OracleGram(d, n_win)
+    rows = uniform_rows(orc, T, d, 100, 0)
+    for b in range(0, T, 100):
+        blk, ts = rows[b:b + 100], np.arange(b + 1, b + 101)
+        ref.update_block(blk, ts)
+        s.update_block(blk, ts)
+        g.add_block(blk, ts)
+        for j in range(s.levels):
+            mine = [(x[1], x[2], x[0]) for x in s.level_state(j).snap_meta()]
+            theirs = [(x["s"], x["t"], x["z"].shape[1]) for x in ref.level_state(j).snaps()]
+            assert mine == theirs, (j, b)
+        q, qr = s.query(), ref.query()
+        assert (q["level"], q["fallback"], q["xi_sum"]) == (qr["level"], qr["fallback"], qr["xi_sum"])
+        assert abs(g.error(q["sketch"]) - g.error(qr["sketch"])) <= 1e-6
+        assert g.error(q["sketch"]) <= eps
