@@ -196,6 +196,11 @@ int aero_dist_theta_schedule(int32_t m, int64_t T, double eps, int64_t latency,
  * the next T ticks of every site's squared norms (m x T row-major) */
 typedef struct aero_dist_protocol aero_dist_protocol;
 int aero_dist_protocol_create(int32_t m, double eps, int64_t latency, aero_dist_protocol** out);
+/* sliding-window protocol (SiteState with window, distributed.cpp:33-55,
+ * 27-30, 107-123): exact per-site window mass, signed FroMass deltas,
+ * theta = eps * own window mass. window = 0 is the whole-stream protocol. */
+int aero_dist_protocol_create_window(int32_t m, double eps, int64_t latency, int64_t window,
+                                     aero_dist_protocol** out);
 int aero_dist_protocol_destroy(aero_dist_protocol* h);
 int aero_dist_protocol_advance(aero_dist_protocol* h, int64_t T, const double* sq_norms,
                                double* theta_out);
@@ -208,6 +213,13 @@ typedef struct aero_coord aero_coord;
 /* coordinator accumulator B (d x d fp64) on `device`; nccl_comm is an
  * ncclComm_t (or NULL for single-process use) */
 int aero_coord_create(int32_t d, int32_t m, int32_t device, void* nccl_comm, aero_coord** out);
+/* CoordinatorState(d, m, window_mode) (distributed.hpp:78-105) with the
+ * simulator's delivery latency (distributed.cpp:226-239): window > 0 keeps a
+ * contribution live from tick t + latency until its Expire is delivered at
+ * t + window + latency (distributed.cpp:87-97, 137-144); absorb() then also
+ * counts the Expire messages' bytes. */
+int aero_coord_create_window(int32_t d, int32_t m, int32_t device, void* nccl_comm, int64_t window,
+                             int64_t latency, aero_coord** out);
 int aero_coord_destroy(aero_coord* h);
 /* CoordinatorState::receive(SnapshotUpdate) for every snapshot queued in the
  * site sketch (distributed.cpp:124-136), popping them (distributed.cpp:74-77);
@@ -219,6 +231,11 @@ int aero_coord_absorb_snapshots(aero_coord* h, aero_sketch* site, int64_t* bytes
  * row-major, nullable) and the d x d Gram (nullable) */
 int aero_coord_probe(aero_coord* h, aero_sketch* const* sites, int32_t nsites, int32_t root,
                      int32_t ell, double* out_ell_by_d, double* out_gram);
+/* shrink_to_sketch (sketch.cpp:167-178) of a merged d x d Gram
+ * given in host memory, on the coordinator's device -> out (ell x d): the
+ * root's last step when the per-rank Grams were summed over a process group
+ * without NCCL (gloo) */
+int aero_coord_shrink(aero_coord* h, const double* gram, int32_t ell, double* out);
 /* NCCL helpers so callers need no NCCL headers: 128-byte unique id */
 int aero_nccl_get_unique_id(char* id128);
 int aero_nccl_comm_init(const char* id128, int32_t nranks, int32_t rank, int32_t device,
@@ -236,6 +253,28 @@ int aero_cod_update_block(aero_cod* h, const double* xs, const double* ys, int64
 int aero_cod_query(aero_cod* h, double* astar, double* bstar);
 int aero_cod_query_product(aero_cod* h, double* p_dx_by_dy);
 int aero_cod_info(aero_cod* h, int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock);
+/* CodState::theta / set_theta (amm.hpp:52-53, amm.cpp:38-41) */
+int aero_cod_theta(aero_cod* h, double* theta);
+int aero_cod_set_theta(aero_cod* h, double theta);
+
+/* ---- AdaptiveState: main/aux CodState pair with queue-length-driven
+ * threshold doubling / halving (amm.hpp:71-93, amm.cpp:131-161).
+ * aero_adaptive_create mirrors AdaptiveState(d_x, d_y, eps, theta0, n,
+ * RngState(seed, stream)); update_block = n sequential update(x, y, i) calls
+ * (xs n x dx, ys n x dy row-major, host); log_out (nullable) receives main's
+ * per-row events, level_out (nullable) level() after each row. Query and
+ * product come from the main sketch (amm.hpp:79). */
+typedef struct aero_adaptive aero_adaptive;
+int aero_adaptive_create(int32_t dx, int32_t dy, double eps, double theta0, int64_t window,
+                         uint64_t seed, uint64_t stream, int32_t device, aero_adaptive** out);
+int aero_adaptive_destroy(aero_adaptive* h);
+int aero_adaptive_update_block(aero_adaptive* h, const double* xs, const double* ys, int64_t n,
+                               const int64_t* t, aero_event* log_out, int32_t* level_out);
+int aero_adaptive_query(aero_adaptive* h, double* astar, double* bstar);
+int aero_adaptive_query_product(aero_adaptive* h, double* p_dx_by_dy);
+/* level(), main().theta(), aux().theta(), main().snaps().size(), aux().snaps().size() */
+int aero_adaptive_info(aero_adaptive* h, int32_t* level, double* theta_main, double* theta_aux,
+                       int64_t* snaps_main, int64_t* snaps_aux);
 
 /* ---- stream generators (BASELINE.json configs; DESIGN.md GENERATOR spec) */
 typedef struct aero_gen_params {

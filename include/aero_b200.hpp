@@ -4,12 +4,14 @@
 //   aero::b200::AttpState   <-> aero::AttpState   (attp.hpp:15-43)
 //   aero::b200::MlState     <-> aero::MlState     (sliding_window.hpp:39-81)
 //   aero::b200::CodState    <-> aero::CodState    (amm.hpp:35-69)
+//   aero::b200::AdaptiveState <-> aero::AdaptiveState (amm.hpp:71-93)
 // Status codes are rethrown as the reference's exception types
 // (errors.hpp:15-33). Vectors are raw pointers / std::vector (row-major), so a
 // maintainer keeps the Eigen call sites by passing a.data().
 #ifndef AERO_B200_HPP
 #define AERO_B200_HPP
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -231,9 +233,47 @@ class CodState {
         return {std::move(a), std::move(b)};
     }
 
+    double theta() const {
+        double t = 0.0;
+        check(aero_cod_theta(h_, &t));
+        return t;
+    }
+    void set_theta(double theta) { check(aero_cod_set_theta(h_, theta)); }
+
   private:
     int dx_, dy_;
     aero_cod* h_ = nullptr;
+};
+
+// AdaptiveState (amm.hpp:71-93): main/aux CodState pair, threshold doubling /
+// halving with main's queue length
+class AdaptiveState {
+  public:
+    AdaptiveState(int dx, int dy, double eps, double theta0, std::int64_t n, std::uint64_t seed,
+                  std::uint64_t stream, int device = 0)
+        : dx_(dx), dy_(dy), ell_(static_cast<int>(std::ceil(2.0 / eps))) {
+        check(aero_adaptive_create(dx, dy, eps, theta0, n, seed, stream, device, &h_));
+    }
+    AdaptiveState(const AdaptiveState&) = delete;
+    AdaptiveState& operator=(const AdaptiveState&) = delete;
+    ~AdaptiveState() { aero_adaptive_destroy(h_); }
+    void update(const double* x, const double* y, std::int64_t i) {
+        check(aero_adaptive_update_block(h_, x, y, 1, &i, nullptr, nullptr));
+    }
+    int level() const {
+        std::int32_t lv = 0;
+        check(aero_adaptive_info(h_, &lv, nullptr, nullptr, nullptr, nullptr));
+        return lv;
+    }
+    std::pair<std::vector<double>, std::vector<double>> query() const {
+        std::vector<double> a((size_t)dx_ * ell_), b((size_t)dy_ * ell_);
+        check(aero_adaptive_query(h_, a.data(), b.data()));
+        return {std::move(a), std::move(b)};
+    }
+
+  private:
+    int dx_, dy_, ell_;
+    aero_adaptive* h_ = nullptr;
 };
 
 }  // namespace b200

@@ -849,6 +849,11 @@ CodState::CodState(int d_x, int d_y, double eps, double theta, std::int64_t n, R
     if (n < 1) throw InvalidInput("CodState: window size must be >= 1");
     ell_ = static_cast<int>(std::ceil(2.0 / eps));
 }
+// reference amm.cpp:38-41
+void CodState::set_theta(double theta) {
+    if (theta < 0.0) throw InvalidInput("CodState: theta must be >= 0");
+    theta_ = theta;
+}
 static Mat append_col(const Mat& m, const double* x) {
     Mat out(m.r, m.c + 1);
     std::memcpy(out.data(), m.data(), sizeof(double) * m.size());
@@ -954,6 +959,36 @@ std::pair<Mat, Mat> CodState::query() const {
         }
     }
     return {std::move(astar), std::move(bstar)};
+}
+
+// reference amm.cpp:131-138. Member order fixes the fork order: main_ takes
+// the parameter's first fork, aux_ its second, rng_ keeps the parent.
+AdaptiveState::AdaptiveState(int d_x, int d_y, double eps, double theta0, std::int64_t n,
+                             RngState rng)
+    : eps_(eps), theta0_(theta0), n_(n), level_(1),
+      main_(d_x, d_y, eps, theta0, n, rng.fork()),
+      aux_(d_x, d_y, eps, theta0, n, rng.fork()),
+      rng_(rng) {
+    if (theta0 <= 0.0) throw InvalidInput("AdaptiveState: theta0 must be > 0");
+}
+// reference amm.cpp:140-159
+void AdaptiveState::update(const double* x, const double* y, std::int64_t i) {
+    if (i > 1 && (i % n_) == 1) {  // window boundary: aux becomes main
+        main_ = aux_;
+        aux_ = CodState(main_.d_x(), main_.d_y(), eps_, main_.theta(), n_, rng_.fork());
+    }
+    main_.update(x, y, i);
+    aux_.update(x, y, i);
+    const double qlen = static_cast<double>(main_.snaps().size());
+    if (qlen >= static_cast<double>(level_) / eps_) {
+        ++level_;
+        main_.set_theta(2.0 * main_.theta());
+        aux_.set_theta(2.0 * aux_.theta());
+    } else if (level_ > 1 && qlen <= static_cast<double>(level_ - 1) / eps_) {
+        --level_;
+        main_.set_theta(0.5 * main_.theta());
+        aux_.set_theta(0.5 * aux_.theta());
+    }
 }
 
 // ---------------------------------------------------------------- exact oracle

@@ -366,7 +366,10 @@ class CodState {
     std::pair<Mat, Mat> query() const;
     Mat query_product() const;  // restored p (dx x dy), pre-SVD
     int ell() const { return ell_; }
+    int d_x() const { return dx_; }
+    int d_y() const { return dy_; }
     double theta() const { return theta_; }
+    void set_theta(double theta);  // amm.cpp:38-41
     std::int64_t clock() const { return clock_; }
     const Mat& a() const { return a_; }
     const Mat& b() const { return b_; }
@@ -384,6 +387,25 @@ class CodState {
     std::int64_t clock_, last_dump_t_;
     RngState rng_;
     Event ev_{};
+};
+
+// main/auxiliary CodState pair with queue-length-driven threshold doubling /
+// halving (reference amm.hpp:71-93, amm.cpp:131-161)
+class AdaptiveState {
+  public:
+    AdaptiveState(int d_x, int d_y, double eps, double theta0, std::int64_t n, RngState rng);
+    void update(const double* x, const double* y, std::int64_t i);
+    std::pair<Mat, Mat> query() const { return main_.query(); }
+    int level() const { return level_; }
+    const CodState& main() const { return main_; }
+    const CodState& aux() const { return aux_; }
+
+  private:
+    double eps_, theta0_;
+    std::int64_t n_;
+    int level_;
+    CodState main_, aux_;
+    RngState rng_;
 };
 
 // ---- exact oracles (reference oracle.hpp:22-130) ----------------------------

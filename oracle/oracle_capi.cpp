@@ -367,6 +367,41 @@ int orc_cod_get_ab(void* h, double* a, double* b) {
     });
 }
 
+// ---- AdaptiveState (reference amm.hpp:71-93)
+void* orc_adaptive_create(int dx, int dy, double eps, double theta0, std::int64_t n,
+                          std::uint64_t seed, std::uint64_t stream) {
+    AdaptiveState* p = nullptr;
+    if (guard([&] { p = new AdaptiveState(dx, dy, eps, theta0, n, RngState(seed, stream)); }) != 0)
+        return nullptr;
+    return p;
+}
+void orc_adaptive_destroy(void* h) { delete static_cast<AdaptiveState*>(h); }
+// per row: level after the row, main's theta and snapshot count after the row
+int orc_adaptive_update_block(void* h, const double* x, const double* y, int dx, int dy,
+                              std::int64_t n, const std::int64_t* t, Event* ev, int* level,
+                              double* theta, std::int64_t* nsnaps) {
+    return guard([&] {
+        auto* s = static_cast<AdaptiveState*>(h);
+        for (std::int64_t q = 0; q < n; ++q) {
+            s->update(x + q * dx, y + q * dy, t[q]);
+            if (ev) ev[q] = s->main().last_event();
+            if (level) level[q] = s->level();
+            if (theta) theta[q] = s->main().theta();
+            if (nsnaps) nsnaps[q] = (std::int64_t)s->main().snaps().size();
+        }
+    });
+}
+int orc_adaptive_query(void* h, double* astar, double* bstar) {
+    return guard([&] {
+        const auto r = static_cast<AdaptiveState*>(h)->query();
+        to_rm(r.first, astar);
+        to_rm(r.second, bstar);
+    });
+}
+int orc_adaptive_query_product(void* h, double* p) {
+    return guard([&] { to_rm(static_cast<AdaptiveState*>(h)->main().query_product(), p); });
+}
+
 // ---- distributed: site / coordinator objects and the tick simulator
 void* orc_site_create(int id, int d, double eps, int m, std::uint64_t seed, std::uint64_t stream,
                       std::int64_t window) {

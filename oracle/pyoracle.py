@@ -144,6 +144,11 @@ def _declare(L):
     d("orc_cod_query_product", i32, vp, dp)
     d("orc_cod_info", i32, vp, ip, lp, lp, lp)
     d("orc_cod_get_ab", i32, vp, dp, dp)
+    d("orc_adaptive_create", vp, i32, i32, f64, f64, i64, u64, u64)
+    d("orc_adaptive_destroy", None, vp)
+    d("orc_adaptive_update_block", i32, vp, dp, dp, i32, i32, i64, lp, P(Event), ip, dp, lp)
+    d("orc_adaptive_query", i32, vp, dp, dp)
+    d("orc_adaptive_query_product", i32, vp, dp)
     d("orc_site_create", vp, i32, i32, f64, i32, u64, u64, i64)
     d("orc_site_destroy", None, vp)
     d("orc_site_update", i32, vp, dp, i64, ip)
@@ -547,6 +552,46 @@ class CodState:
         a, b = np.empty((self.dx, cols)), np.empty((self.dy, cols))
         _chk(lib().orc_cod_get_ab(self._h, _dp(a), _dp(b)))
         return a, b
+
+
+class AdaptiveState:
+    """reference amm.hpp:71-93 / amm.cpp:131-161 (main/aux CodState pair with
+    queue-length-driven threshold doubling and halving)."""
+
+    def __init__(self, dx, dy, eps, theta0, n, seed=0, stream=0):
+        h = lib().orc_adaptive_create(dx, dy, eps, theta0, n, seed, stream)
+        if not h:
+            raise InvalidInput(lib().orc_last_error().decode())
+        self._h, self.dx, self.dy, self.ell = h, dx, dy, int(np.ceil(2.0 / eps))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_adaptive_destroy(self._h)
+            self._h = None
+
+    def update_block(self, xs, ys, ts):
+        """-> (main's events, level, main theta, main snapshot count) per row."""
+        xs, ys = _f64(xs), _f64(ys)
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = xs.shape[0]
+        ev = (Event * max(n, 1))()
+        lv = np.zeros(max(n, 1), np.int32)
+        th = np.zeros(max(n, 1))
+        ns = np.zeros(max(n, 1), np.int64)
+        _chk(lib().orc_adaptive_update_block(self._h, _dp(xs), _dp(ys), self.dx, self.dy, n, _lp(ts), ev,
+                                             lv.ctypes.data_as(P(i32)), _dp(th), _lp(ns)))
+        return dict(events=np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy(), level=lv[:n],
+                    theta=th[:n], nsnaps=ns[:n])
+
+    def query(self):
+        a, b = np.empty((self.dx, self.ell)), np.empty((self.dy, self.ell))
+        _chk(lib().orc_adaptive_query(self._h, _dp(a), _dp(b)))
+        return a, b
+
+    def query_product(self):
+        p = np.empty((self.dx, self.dy))
+        _chk(lib().orc_adaptive_query_product(self._h, _dp(p)))
+        return p
 
 
 MSG_KINDS = ("FroMass", "FroBroadcast", "SnapshotUpdate", "Expire")

@@ -156,6 +156,17 @@ SIGNATURES = [
     ("aero_cod_query", i32, [vp, P(f64), P(f64)]),
     ("aero_cod_query_product", i32, [vp, P(f64)]),
     ("aero_cod_info", i32, [vp, P(i32), P(i64), P(i64), P(i64)]),
+    ("aero_dist_protocol_create_window", i32, [i32, f64, i64, i64, P(vp)]),
+    ("aero_coord_create_window", i32, [i32, i32, i32, vp, i64, i64, P(vp)]),
+    ("aero_coord_shrink", i32, [vp, P(f64), i32, P(f64)]),
+    ("aero_cod_theta", i32, [vp, P(f64)]),
+    ("aero_cod_set_theta", i32, [vp, f64]),
+    ("aero_adaptive_create", i32, [i32, i32, f64, f64, i64, u64, u64, i32, P(vp)]),
+    ("aero_adaptive_destroy", i32, [vp]),
+    ("aero_adaptive_update_block", i32, [vp, P(f64), P(f64), i64, P(i64), P(Event), P(i32)]),
+    ("aero_adaptive_query", i32, [vp, P(f64), P(f64)]),
+    ("aero_adaptive_query_product", i32, [vp, P(f64)]),
+    ("aero_adaptive_info", i32, [vp, P(i32), P(f64), P(f64), P(i64), P(i64)]),
     ("aero_gen_rows_device", i32, [P(GenParams), i64, i64, vp, i32]),
     ("aero_last_error", C.c_char_p, []),
     ("aero_version", C.c_char_p, []),
@@ -606,6 +617,72 @@ class CodState:
         _chk(lib().aero_cod_query_product(self._h, _dp(p)))
         return p
 
+    @property
+    def theta(self):
+        th = f64()
+        _chk(lib().aero_cod_theta(self._h, C.byref(th)))
+        return th.value
+
+    def set_theta(self, theta):
+        _chk(lib().aero_cod_set_theta(self._h, theta))
+
+
+class AdaptiveState:
+    """reference AdaptiveState (amm.hpp:71-93, amm.cpp:131-161): main/auxiliary
+    CodState pair whose threshold doubles / halves with main's queue length;
+    the auxiliary sketch, rebuilt from each window boundary, replaces the main
+    one every n rows."""
+
+    def __init__(self, dx, dy, eps, theta0, n, seed=0, stream=0, device=0):
+        h = vp()
+        _chk(lib().aero_adaptive_create(dx, dy, eps, theta0, n, seed, stream, device, C.byref(h)))
+        self._h, self.dx, self.dy, self.ell = h, dx, dy, int(np.ceil(2.0 / eps))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_adaptive_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        lv, tm, ta, sm, sa = i32(), f64(), f64(), i64(), i64()
+        _chk(lib().aero_adaptive_info(self._h, C.byref(lv), C.byref(tm), C.byref(ta), C.byref(sm), C.byref(sa)))
+        return dict(level=lv.value, theta_main=tm.value, theta_aux=ta.value, snaps_main=sm.value,
+                    snaps_aux=sa.value)
+
+    @property
+    def level(self):
+        return self.info()["level"]
+
+    def update_block(self, xs, ys, ts):
+        """-> (main's per-row events, level() after each row)."""
+        xs, ys = _f64(xs), _f64(ys)
+        if xs.ndim != 2 or ys.ndim != 2 or xs.shape[1] != self.dx or ys.shape[1] != self.dy:
+            raise InvalidInput("CodState: dimension mismatch")
+        ts = np.ascontiguousarray(ts, np.int64)
+        n = ts.shape[0]
+        _check_block(xs.shape[0], n)
+        _check_block(ys.shape[0], n)
+        ev = (Event * max(n, 1))()
+        lv = np.zeros(max(n, 1), np.int32)
+        _chk(lib().aero_adaptive_update_block(self._h, _dp(xs), _dp(ys), n, _lp(ts), ev, lv.ctypes.data_as(P(i32))))
+        return np.frombuffer(ev, dtype=EVENT_DTYPE, count=n).copy(), lv[:n].copy()
+
+    def query(self):
+        a, b = np.empty((self.dx, self.ell)), np.empty((self.dy, self.ell))
+        _chk(lib().aero_adaptive_query(self._h, _dp(a), _dp(b)))
+        return a, b
+
+    def query_product(self):
+        p = np.empty((self.dx, self.dy))
+        _chk(lib().aero_adaptive_query_product(self._h, _dp(p)))
+        return p
+
 
 def dist_theta_schedule(sq_norms, eps, latency=0):
     """Per-site thresholds from the norm-only protocol replay
@@ -619,12 +696,13 @@ def dist_theta_schedule(sq_norms, eps, latency=0):
 
 
 class DistProtocol:
-    """Streaming norm-only replay of the whole-stream mass protocol
-    (distributed.cpp:31-69, 107-123, 201-239): per-site thresholds per tick."""
+    """Streaming norm-only replay of the mass protocol (distributed.cpp:31-69,
+    107-123, 201-239): per-site thresholds per tick; window > 0 = the
+    sliding-window protocol (distributed.cpp:33-55)."""
 
-    def __init__(self, m, eps, latency=0):
+    def __init__(self, m, eps, latency=0, window=0):
         h = vp()
-        _chk(lib().aero_dist_protocol_create(m, eps, latency, C.byref(h)))
+        _chk(lib().aero_dist_protocol_create_window(m, eps, latency, window or 0, C.byref(h)))
         self._h, self.m = h, m
 
     def close(self):
@@ -664,9 +742,9 @@ class Coordinator:
     """reference CoordinatorState (distributed.hpp:78-105) as a device
     accumulator per rank, merged with ncclReduce at probe time."""
 
-    def __init__(self, d, m, device=0, nccl_comm=None):
+    def __init__(self, d, m, device=0, nccl_comm=None, window=0, latency=0):
         h = vp()
-        _chk(lib().aero_coord_create(d, m, device, nccl_comm, C.byref(h)))
+        _chk(lib().aero_coord_create_window(d, m, device, nccl_comm, window or 0, latency, C.byref(h)))
         self._h, self.d = h, d
 
     def close(self):
@@ -691,6 +769,13 @@ class Coordinator:
         gram = np.empty((self.d, self.d)) if want_gram else None
         _chk(lib().aero_coord_probe(self._h, arr, len(sites), root, ell, _dp(out), _dp(gram)))
         return out, gram
+
+    def shrink(self, gram, ell):
+        """shrink_to_sketch of a host-merged Gram on this coordinator's device."""
+        g = _f64(gram)
+        out = np.empty((ell, self.d))
+        _chk(lib().aero_coord_shrink(self._h, _dp(g), ell, _dp(out)))
+        return out
 
 
 def nccl_unique_id() -> bytes:

@@ -391,6 +391,11 @@ int aero_dist_protocol_create(int32_t m, double eps, int64_t latency, aero_dist_
     REQ(out);
     return guard([&] { *out = new aero_dist_protocol{new DistProtocol(m, eps, latency)}; });
 }
+int aero_dist_protocol_create_window(int32_t m, double eps, int64_t latency, int64_t window,
+                                     aero_dist_protocol** out) {
+    REQ(out);
+    return guard([&] { *out = new aero_dist_protocol{new DistProtocol(m, eps, latency, window)}; });
+}
 int aero_dist_protocol_destroy(aero_dist_protocol* h) {
     if (!h) return AERO_OK;
     delete h->p;
@@ -439,6 +444,11 @@ int aero_coord_create(int32_t d, int32_t m, int32_t device, void* nccl_comm, aer
     REQ(out);
     return guard([&] { *out = new aero_coord{new Coordinator(d, m, device, nccl_comm)}; });
 }
+int aero_coord_create_window(int32_t d, int32_t m, int32_t device, void* nccl_comm, int64_t window,
+                             int64_t latency, aero_coord** out) {
+    REQ(out);
+    return guard([&] { *out = new aero_coord{new Coordinator(d, m, device, nccl_comm, window, latency)}; });
+}
 int aero_coord_destroy(aero_coord* h) {
     if (!h) return AERO_OK;
     return guard([&] {
@@ -463,6 +473,12 @@ int aero_coord_probe(aero_coord* h, aero_sketch* const* sites, int32_t nsites, i
             if (sites && sites[i]) ss.push_back(sites[i]->s);
         h->c->probe(ss, root, ell, out, gram);
     });
+}
+int aero_coord_shrink(aero_coord* h, const double* gram, int32_t ell, double* out) {
+    REQ(h);
+    REQ(gram);
+    REQ(out);
+    return guard([&] { h->c->shrink(gram, ell, out); });
 }
 int aero_nccl_get_unique_id(char* id128) {
     REQ(id128);
@@ -515,6 +531,67 @@ int aero_cod_query_product(aero_cod* h, double* p) {
 int aero_cod_info(aero_cod* h, int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock) {
     REQ(h);
     h->e->info(ell, cols, snaps, clock);
+    return AERO_OK;
+}
+
+int aero_cod_theta(aero_cod* h, double* theta) {
+    REQ(h);
+    REQ(theta);
+    *theta = h->e->theta();
+    return AERO_OK;
+}
+int aero_cod_set_theta(aero_cod* h, double theta) {
+    REQ(h);
+    return guard([&] { h->e->set_theta(theta); });
+}
+
+// ---- AdaptiveState -------------------------------------------------------------
+struct aero_adaptive {
+    AdaptiveEngine* e;
+};
+int aero_adaptive_create(int32_t dx, int32_t dy, double eps, double theta0, int64_t window,
+                         uint64_t seed, uint64_t stream, int32_t device, aero_adaptive** out) {
+    REQ(out);
+    return guard([&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw CudaError("no CUDA device: the AeroSketch B200 path has no CPU fallback");
+        *out = new aero_adaptive{new AdaptiveEngine(dx, dy, eps, theta0, window, seed, stream, device)};
+    });
+}
+int aero_adaptive_destroy(aero_adaptive* h) {
+    if (!h) return AERO_OK;
+    return guard([&] {
+        delete h->e;
+        delete h;
+    });
+}
+int aero_adaptive_update_block(aero_adaptive* h, const double* xs, const double* ys, int64_t n,
+                               const int64_t* t, aero_event* log_out, int32_t* level_out) {
+    REQ(h);
+    if (n > 0) {
+        REQ(xs);
+        REQ(ys);
+        REQ(t);
+    }
+    return guard([&] { h->e->update_block(xs, ys, n, t, log_out, level_out); });
+}
+int aero_adaptive_query(aero_adaptive* h, double* astar, double* bstar) {
+    REQ(h);
+    return guard([&] { h->e->main().query(astar, bstar); });
+}
+int aero_adaptive_query_product(aero_adaptive* h, double* p) {
+    REQ(h);
+    return guard([&] { h->e->main().query_product(p); });
+}
+int aero_adaptive_info(aero_adaptive* h, int32_t* level, double* theta_main, double* theta_aux,
+                       int64_t* snaps_main, int64_t* snaps_aux) {
+    REQ(h);
+    if (level) *level = h->e->level();
+    if (theta_main) *theta_main = h->e->main().theta();
+    if (theta_aux) *theta_aux = h->e->aux().theta();
+    if (snaps_main) *snaps_main = h->e->main().snap_count();
+    if (snaps_aux) *snaps_aux = h->e->aux().snap_count();
     return AERO_OK;
 }
 

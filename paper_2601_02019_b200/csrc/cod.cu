@@ -897,4 +897,92 @@ void CodEngine::info(int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock
     if (clock) *clock = im_->clock;
 }
 
+double CodEngine::theta() const { return im_->theta; }
+void CodEngine::set_theta(double theta) {
+    if (theta < 0.0) throw InvalidInput("CodState: theta must be >= 0");
+    im_->theta = theta;
+}
+int64_t CodEngine::window() const { return im_->n; }
+int64_t CodEngine::snap_count() const { return (int64_t)im_->snaps.size(); }
+int64_t CodEngine::snap_t(int64_t idx) const { return im_->snaps[(size_t)idx].t; }
+
+// ============================================================================
+// AdaptiveState
+// ============================================================================
+// amm.cpp:131-138: main_ takes the constructor rng's first fork, aux_ its
+// second; rng_ keeps the parent (forks = 2) for the boundary re-creations.
+AdaptiveEngine::AdaptiveEngine(int dx, int dy, double eps, double theta0, int64_t n, uint64_t seed,
+                               uint64_t stream, int device)
+    : dx_(dx), dy_(dy), dev_(device), eps_(eps), n_(n), seed_(seed), stream_(stream) {
+    main_ = std::make_unique<CodEngine>(dx, dy, eps, theta0, n, seed, fork_stream(stream, ++forks_), device);
+    aux_ = std::make_unique<CodEngine>(dx, dy, eps, theta0, n, seed, fork_stream(stream, ++forks_), device);
+    if (theta0 <= 0.0) throw InvalidInput("AdaptiveState: theta0 must be > 0");
+}
+
+// amm.cpp:140-159, one chunk of rows at a time. A chunk [q, e) starts at a
+// window boundary or right after an adaptation check and ends
+//  * before the next boundary row (the swap precedes that row's update),
+//  * at the first row where the main queue could reach level/eps: it grows by
+//    at most one snapshot per row (one dump per update),
+//  * at the first row where it could fall to (level-1)/eps: the queue never
+//    holds fewer than the already-queued snapshots still inside the window.
+// Only the chunk's last row can therefore trigger the rule, which is applied
+// once after it exactly as after every row of the reference.
+void AdaptiveEngine::update_block(const double* xs, const double* ys, int64_t nrows, const int64_t* t,
+                                  aero_event* log, int32_t* level_out) {
+    int64_t q = 0;
+    while (q < nrows) {
+        const int64_t i = t[q];
+        if (i > 1 && (i % n_) == 1) {  // amm.cpp:143-146: aux becomes main
+            const double th = aux_->theta();
+            main_ = std::move(aux_);
+            aux_ = std::make_unique<CodEngine>(dx_, dy_, eps_, th, n_, seed_, fork_stream(stream_, ++forks_), dev_);
+        }
+        const int64_t qlen0 = main_->snap_count();
+        const double up = static_cast<double>(level_) / eps_;
+        const double down = static_cast<double>(level_ - 1) / eps_;
+        int64_t e = q + 1, first_live = 0;
+        for (; e < nrows; ++e) {
+            const int64_t j = e - 1;  // row j is inside the chunk; may row e join it?
+            const int64_t tr = t[e];
+            if (tr > 1 && (tr % n_) == 1) break;                       // boundary before row e
+            if (static_cast<double>(qlen0 + (j - q + 1)) >= up) break;  // row j may reach `up`
+            if (level_ > 1) {  // queued snapshots still live after row j (t_s + n > t_j)
+                while (first_live < qlen0 && main_->snap_t(first_live) + n_ <= t[j]) ++first_live;
+                if (static_cast<double>(qlen0 - first_live) <= down) break;
+            }
+        }
+        try {
+            main_->update_block(xs + q * dx_, ys + q * dy_, e - q, t + q, log ? log + q : nullptr);
+        } catch (...) {
+            // the reference's aux_ saw every row before the failing one
+            // (amm.cpp:147-148); no row before it was an adaptation point
+            int64_t clk = 0, good = 0;
+            main_->info(nullptr, nullptr, nullptr, &clk);
+            while (q + good < e && t[q + good] <= clk) ++good;
+            if (good > 0) aux_->update_block(xs + q * dx_, ys + q * dy_, good, t + q, nullptr);
+            if (level_out)
+                for (int64_t r = q; r < q + good; ++r) level_out[r] = level_;
+            throw;
+        }
+        aux_->update_block(xs + q * dx_, ys + q * dy_, e - q, t + q, nullptr);
+        const int lv0 = level_;
+        const double qlen = static_cast<double>(main_->snap_count());
+        if (qlen >= up) {
+            ++level_;
+            main_->set_theta(2.0 * main_->theta());
+            aux_->set_theta(2.0 * aux_->theta());
+        } else if (level_ > 1 && qlen <= down) {
+            --level_;
+            main_->set_theta(0.5 * main_->theta());
+            aux_->set_theta(0.5 * aux_->theta());
+        }
+        if (level_out) {
+            for (int64_t r = q; r + 1 < e; ++r) level_out[r] = lv0;
+            level_out[e - 1] = level_;
+        }
+        q = e;
+    }
+}
+
 }  // namespace aero_b200

@@ -297,39 +297,60 @@ void MlEngine::heavy_get(int j, int64_t idx, double* row, int64_t* s, int64_t* t
 // for the site side, :107-123 for the coordinator, :201-239 for the tick loop
 // and FIFO latencies). Snapshot messages ride the same FIFO but never change
 // the mass estimate, so every site's threshold is a function of norms alone.
-DistProtocol::DistProtocol(int m, double eps, int64_t latency)
-    : m_(m), eps_(eps), latency_(latency), f_local_(m > 0 ? m : 0, 0.0),
-      f_self_(m > 0 ? m : 0, 0.0), f_known_(m > 0 ? m : 0, 0.0) {
+DistProtocol::DistProtocol(int m, double eps, int64_t latency, int64_t window)
+    : m_(m), eps_(eps), latency_(latency), window_(window), f_local_(m > 0 ? m : 0, 0.0),
+      f_self_(m > 0 ? m : 0, 0.0), f_known_(m > 0 ? m : 0, 0.0), w_local_(m > 0 ? m : 0, 0.0),
+      w_sent_(m > 0 ? m : 0, 0.0), ring_(window > 0 && m > 0 ? m : 0) {
     if (m < 1) throw InvalidInput("run_simulation: m must be >= 1");
     if (!(eps > 0.0 && eps <= 1.0)) throw InvalidInput("run_simulation: eps out of (0,1]");
     if (latency < 0) throw InvalidInput("run_simulation: latency must be >= 0");
+    if (window < 0) throw InvalidInput("run_simulation: window must be >= 0");
 }
 
 // ticks ticks+1 .. ticks+T; site j's norms at sq_norms[j * T + q]
 void DistProtocol::advance(int64_t T, const double* sq_norms, double* theta_out) {
     const int m = m_;
     const double eps = eps_;
+    const bool win = window_ > 0;
     for (int64_t q = 0; q < T; ++q) {
         const int64_t i = ticks + q + 1;
         while (!to_sites_.empty() && to_sites_.front().first <= i) {  // distributed.cpp:211-215
-            for (int j = 0; j < m; ++j) f_known_[j] = std::max(f_known_[j], to_sites_.front().second);
+            const double fb = to_sites_.front().second;
+            for (int j = 0; j < m; ++j) f_known_[j] = win ? fb : std::max(f_known_[j], fb);  // :27-30
             to_sites_.pop_front();
         }
-        for (int j = 0; j < m; ++j) {  // SiteState::update, distributed.cpp:57-69
+        for (int j = 0; j < m; ++j) {
             const double nsq = sq_norms[(int64_t)j * T + q];
-            f_local_[j] += nsq;
-            if (f_local_[j] >= (eps / m) * f_known_[j]) {
-                to_coord_.emplace_back(i + latency_, f_local_[j]);
-                bytes += 8 + 16;
-                f_self_[j] += f_local_[j];
-                f_local_[j] = 0.0;
+            if (win) {  // SiteState::update, distributed.cpp:33-55
+                std::deque<double>& ring = ring_[j];
+                ring.push_back(nsq);
+                w_local_[j] += nsq;
+                while ((int64_t)ring.size() > window_) {
+                    w_local_[j] -= ring.front();
+                    ring.pop_front();
+                }
+                const double delta = w_local_[j] - w_sent_[j];
+                if (std::abs(delta) >= (eps / m) * f_known_[j]) {
+                    to_coord_.emplace_back(i + latency_, delta);
+                    bytes += 8 + 16;
+                    w_sent_[j] = w_local_[j];
+                }
+                theta_out[(int64_t)j * T + q] = eps * w_local_[j];
+            } else {  // SiteState::update, distributed.cpp:57-69
+                f_local_[j] += nsq;
+                if (f_local_[j] >= (eps / m) * f_known_[j]) {
+                    to_coord_.emplace_back(i + latency_, f_local_[j]);
+                    bytes += 8 + 16;
+                    f_self_[j] += f_local_[j];
+                    f_local_[j] = 0.0;
+                }
+                theta_out[(int64_t)j * T + q] = eps * std::max(f_known_[j], f_self_[j] + f_local_[j]);
             }
-            theta_out[(int64_t)j * T + q] = eps * std::max(f_known_[j], f_self_[j] + f_local_[j]);
         }
         while (!to_coord_.empty() && to_coord_.front().first <= i) {  // distributed.cpp:231-239
             const double f = to_coord_.front().second;
             to_coord_.pop_front();
-            if (!(f >= 0.0)) throw ProtocolError("FroMass: negative mass");
+            if (!win && !(f >= 0.0)) throw ProtocolError("FroMass: negative mass");
             f_hat = std::max(f_hat + f, 0.0);  // CoordinatorState::receive, :109-123
             if (++msg_count_ >= m) {
                 msg_count_ = 0;
@@ -350,9 +371,11 @@ void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const do
     if (broadcasts) *broadcasts = p.broadcasts;
 }
 
-Coordinator::Coordinator(int d, int m, int device, void* comm) : d_(d), m_(m), dev_(device), comm_(comm) {
+Coordinator::Coordinator(int d, int m, int device, void* comm, int64_t window, int64_t latency)
+    : d_(d), m_(m), dev_(device), comm_(comm), window_(window), latency_(latency) {
     if (d < 1) throw InvalidInput("CoordinatorState: d must be >= 1");
     if (m < 1) throw InvalidInput("CoordinatorState: site count must be >= 1");
+    if (window < 0 || latency < 0) throw InvalidInput("CoordinatorState: window and latency must be >= 0");
     AERO_CUDA(cudaSetDevice(dev_));
     AERO_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     B_.alloc((size_t)d * d);
@@ -367,14 +390,41 @@ Coordinator::~Coordinator() {
         cudaStreamDestroy(st_);
     }
 }
-// CoordinatorState::receive(SnapshotUpdate) for each queued snapshot
-// (distributed.cpp:124-136) after the site ships them (distributed.cpp:74-85)
+Coordinator::SiteBook& Coordinator::book(const Sketch* s) {
+    for (auto& kv : books_)
+        if (kv.first == s) return kv.second;
+    books_.emplace_back(s, SiteBook{});
+    return books_.back().second;
+}
+// The site ships every snapshot as it is produced (distributed.cpp:74-85);
+// bytes = Message::bytes (distributed.hpp:33-42). Whole-stream mode folds the
+// delivered ones (t + latency <= clock) into B (CoordinatorState::receive,
+// distributed.cpp:124-136). Window mode also counts the Expire notices sent by
+// the site's update at tick t + window (distributed.cpp:87-97) and drops the
+// contributions whose Expire has been delivered (t + window + latency <= clock).
 int64_t Coordinator::absorb(Sketch& site) {
     if (site.d() != d_) throw ProtocolError("SnapshotUpdate: inconsistent payload shapes");
     AERO_CUDA(cudaSetDevice(dev_));
-    const int64_t ns = site.snap_count();
+    SiteBook& bk = book(&site);
+    const int64_t clock = site.clock();
     int64_t bytes = 0;
-    for (int64_t i = 0; i < ns; ++i) bytes += 8 * (2 * (int64_t)d_ * site.snaps()[i].xi) + 16;
+    for (const SnapRec& r : site.snaps()) {
+        if (r.t <= bk.shipped_t) continue;
+        bytes += 8 * (2 * (int64_t)d_ * r.xi) + 16;
+        if (window_ > 0) bk.unexpired.push_back(r.t);
+    }
+    if (!site.snaps().empty()) bk.shipped_t = std::max(bk.shipped_t, site.snaps().back().t);
+    if (window_ > 0) {
+        while (!bk.unexpired.empty() && bk.unexpired.front() + window_ <= clock) {
+            bytes += 8 + 16;  // Expire
+            bk.unexpired.pop_front();
+        }
+        while (site.snap_count() > 0 && site.snaps().front().t + window_ + latency_ <= clock)
+            site.snap_pop_front();
+        return bytes;
+    }
+    int64_t ns = 0;
+    while (ns < site.snap_count() && site.snaps()[ns].t + latency_ <= clock) ++ns;
     if (ns > 0) {
         site.synchronize();
         site.accumulate_restore(B_.p, 0, ns);  // on the site's stream
@@ -391,6 +441,15 @@ void Coordinator::probe(const std::vector<Sketch*>& sites, int root, int ell, do
     AERO_CUDA(cudaStreamSynchronize(st_));
     for (Sketch* site : sites) {  // residual Grams (distributed.cpp:162-165)
         site->accumulate_residual(P_.p, 1.0);
+        if (window_ > 0) {  // live (delivered, unexpired) contributions (:166-172)
+            const int64_t clock = site->clock();
+            int64_t lo = 0, hi = 0;
+            const int64_t ns = site->snap_count();
+            while (lo < ns && site->snaps()[lo].t + window_ + latency_ <= clock) ++lo;
+            hi = lo;
+            while (hi < ns && site->snaps()[hi].t + latency_ <= clock) ++hi;
+            if (hi > lo) site->accumulate_restore(P_.p, lo, hi);
+        }
         site->synchronize();
     }
     double* G = P_.p;
@@ -414,6 +473,17 @@ void Coordinator::probe(const std::vector<Sketch*>& sites, int root, int ell, do
             AERO_CUDA(cudaMemcpyAsync(out_host, out_.p, sizeof(double) * ell * d_, cudaMemcpyDeviceToHost, st_));
         }
     }
+    AERO_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Coordinator::shrink(const double* gram_host, int ell, double* out_host) {
+    if (ell < 1) throw InvalidInput("shrink_to_sketch: ell must be >= 1");
+    AERO_CUDA(cudaSetDevice(dev_));
+    P_.alloc((size_t)d_ * d_);
+    out_.alloc((size_t)ell * d_ + d_);
+    AERO_CUDA(cudaMemcpyAsync(P_.p, gram_host, sizeof(double) * d_ * d_, cudaMemcpyHostToDevice, st_));
+    shrink_device(st_, d_, ell, P_.p, out_.p + (size_t)ell * d_, out_.p);
+    AERO_CUDA(cudaMemcpyAsync(out_host, out_.p, sizeof(double) * ell * d_, cudaMemcpyDeviceToHost, st_));
     AERO_CUDA(cudaStreamSynchronize(st_));
 }
 

@@ -56,7 +56,10 @@ void dist_theta_schedule(int m, int64_t T, double eps, int64_t latency, const do
 // streaming form of the replay (state persists across advance() calls)
 class DistProtocol {
   public:
-    DistProtocol(int m, double eps, int64_t latency);
+    // window > 0: sliding-window protocol (distributed.cpp:33-55: exact
+    // window mass per site, signed FroMass deltas, theta = eps * own window
+    // mass; the broadcast replaces the estimate, distributed.cpp:27-30)
+    DistProtocol(int m, double eps, int64_t latency, int64_t window = 0);
     void advance(int64_t T, const double* sq_norms, double* theta_out);
     int64_t ticks = 0, bytes = 0, broadcasts = 0;
     double f_hat = 0.0;
@@ -64,21 +67,41 @@ class DistProtocol {
   private:
     int m_;
     double eps_;
-    int64_t latency_;
-    std::vector<double> f_local_, f_self_, f_known_;
+    int64_t latency_, window_;
+    std::vector<double> f_local_, f_self_, f_known_, w_local_, w_sent_;
+    std::vector<std::deque<double>> ring_;
     int msg_count_ = 0;
     std::deque<std::pair<int64_t, double>> to_coord_, to_sites_;
 };
+// The coordinator's share on one rank. Whole-stream mode: shipped snapshots
+// are folded into one fp64 d x d accumulator (CoordinatorState::receive,
+// distributed.cpp:124-136). Sliding-window mode: a contribution lives from its
+// delivery (t + latency) until its Expire message is delivered
+// (t + window + latency, distributed.cpp:87-97,137-144); the live snapshots
+// stay factored in the site's own queue (the coordinator's cache) and a probe
+// restores them, so an expiry is a queue pop, not a d x d subtraction.
 class Coordinator {
   public:
-    Coordinator(int d, int m, int device, void* nccl_comm);
+    Coordinator(int d, int m, int device, void* nccl_comm, int64_t window = 0, int64_t latency = 0);
     ~Coordinator();
+    // ship the site's snapshots up to its clock; returns the protocol bytes of
+    // the SnapshotUpdate (and, window mode, Expire) messages sent since the last call
     int64_t absorb(Sketch& site);
     void probe(const std::vector<Sketch*>& sites, int root, int ell, double* out_host, double* gram_host);
+    // shrink_to_sketch of a merged Gram supplied by the host (a merge done
+    // over a non-NCCL process group)
+    void shrink(const double* gram_host, int ell, double* out_host);
 
   private:
     int d_, m_, dev_;
     void* comm_;
+    int64_t window_, latency_;
+    struct SiteBook {
+        int64_t shipped_t = 0;  // snapshots with t <= shipped_t were counted as sent
+        std::deque<int64_t> unexpired;  // shipped snapshot times whose Expire is not sent yet
+    };
+    std::vector<std::pair<const Sketch*, SiteBook>> books_;
+    SiteBook& book(const Sketch* s);
     DeviceBuf B_, P_, W_, out_;
     cudaStream_t st_ = nullptr;
 };
@@ -97,10 +120,40 @@ class CodEngine {
     void query(double* astar, double* bstar);
     void query_product(double* p);
     void info(int32_t* ell, int64_t* cols, int64_t* snaps, int64_t* clock) const;
+    double theta() const;
+    void set_theta(double theta);  // amm.cpp:38-41
+    int64_t window() const;
+    int64_t snap_count() const;
+    int64_t snap_t(int64_t idx) const;  // queue order (oldest first)
 
   private:
     struct Impl;
     Impl* im_;
+};
+
+// ---- AdaptiveState (amm.hpp:71-93, amm.cpp:131-161) ------------------------
+// main/auxiliary CodEngine pair; the threshold doubles / halves with the main
+// queue length. Rows run through both engines in chunks that provably contain
+// no adaptation point except possibly their last row (the queue grows by at
+// most one snapshot per row, and expiry is known from the snapshot times), so
+// each engine keeps its speculative row batches.
+class AdaptiveEngine {
+  public:
+    AdaptiveEngine(int dx, int dy, double eps, double theta0, int64_t n, uint64_t seed,
+                   uint64_t stream, int device);
+    void update_block(const double* xs, const double* ys, int64_t n, const int64_t* t,
+                      aero_event* log, int32_t* level_out);
+    CodEngine& main() { return *main_; }
+    CodEngine& aux() { return *aux_; }
+    int level() const { return level_; }
+
+  private:
+    int dx_, dy_, dev_;
+    double eps_;
+    int64_t n_;
+    int level_ = 1;
+    uint64_t seed_, stream_, forks_ = 0;  // rng_ of amm.hpp:92 (parent stream)
+    std::unique_ptr<CodEngine> main_, aux_;
 };
 
 // ---- generator ---------------------------------------------------------------

@@ -36,10 +36,11 @@ class ThresholdExchange:
     """All-gather of per-site squared norms + deterministic protocol replay.
     Host-only (works with gloo or nccl process groups)."""
 
-    def __init__(self, m: int, eps: float, rank: int = 0, world: int = 1, group=None, latency: int = 0):
+    def __init__(self, m: int, eps: float, rank: int = 0, world: int = 1, group=None, latency: int = 0,
+                 window: int = 0):
         self.m, self.eps, self.rank, self.world, self.group = m, eps, rank, world, group
         self.local = sites_of(rank, world, m)
-        self.proto = DistProtocol(m, eps, latency)
+        self.proto = DistProtocol(m, eps, latency, window)
 
     def gather(self, local_norms: dict[int, np.ndarray]) -> np.ndarray:
         T = len(next(iter(local_norms.values()))) if local_norms else 0
@@ -77,9 +78,14 @@ class DistributedSketch:
     """The sites hosted by this rank plus its share of the coordinator."""
 
     def __init__(self, d: int, eps: float, m: int, seed: int = 0, rank: int = 0, world: int = 1,
-                 group=None, device: int = 0, use_nccl: bool | None = None, latency: int = 0):
+                 group=None, device: int = 0, use_nccl: bool | None = None, latency: int = 0,
+                 window: int = 0):
+        """window > 0: the sliding-window protocol (SiteState with a window,
+        distributed.cpp:33-55, 87-97; CoordinatorState(window_mode=true),
+        :137-144)."""
         self.d, self.eps, self.m, self.rank, self.world, self.device = d, eps, m, rank, world, device
-        self.exchange = ThresholdExchange(m, eps, rank, world, group, latency)
+        self.window = window or 0
+        self.exchange = ThresholdExchange(m, eps, rank, world, group, latency, self.window)
         self.sites = {j: AeroState(d, eps, 0.0, seed=seed, stream=SKETCH_STREAM_BASE + j, device=device)
                       for j in self.exchange.local}
         self.ell = next(iter(self.sites.values())).ell if self.sites else int(np.ceil(2.0 / eps))
@@ -88,7 +94,7 @@ class DistributedSketch:
             use_nccl = world > 1
         if use_nccl:
             self._comm = self._nccl_comm(group)
-        self.coord = Coordinator(d, m, device, self._comm)
+        self.coord = Coordinator(d, m, device, self._comm, window=self.window, latency=latency)
         self.snapshot_bytes = 0
         self.clock = 0
 
@@ -122,10 +128,28 @@ class DistributedSketch:
             self.snapshot_bytes += self.coord.absorb(self.sites[j])
         self.clock = t0 + T - 1
 
-    def probe(self, want_gram: bool = False, root: int = 0):
-        """Merged sketch (ell x d) and optionally the d x d Gram on `root`."""
-        return self.coord.probe(list(self.sites.values()), self.ell, root=root, want_gram=want_gram)
+    def probe(self, want_gram: bool = False, root: int = 0, group=None):
+        """Merged sketch (ell x d) and optionally the d x d Gram on `root`.
+
+        With an NCCL communicator the per-rank Grams meet in one ncclReduce
+        inside the library. Over a process group without NCCL (gloo, e.g.
+        ranks sharing a GPU or a host-side test harness) each rank's Gram is
+        summed with torch.distributed.reduce and the root shrinks it on its
+        device; either way the merge is probe_gram (distributed.cpp:159-173)."""
+        sites = list(self.sites.values())
+        if self.world == 1 or self._comm is not None:
+            return self.coord.probe(sites, self.ell, root=root, want_gram=want_gram)
+        import torch
+        import torch.distributed as dist
+        _, g = self.coord.probe(sites, 0, root=0, want_gram=True)  # this rank only (no comm)
+        t = torch.from_numpy(g)
+        dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
+        if self.rank != root:
+            return None, None
+        g = t.numpy()
+        return self.coord.shrink(g, self.ell), (g if want_gram else None)
 
     def comm_bytes_local(self) -> int:
-        """Snapshot message bytes shipped by this rank's sites."""
+        """SnapshotUpdate (and, window mode, Expire) message bytes shipped by
+        this rank's sites."""
         return self.snapshot_bytes

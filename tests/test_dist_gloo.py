@@ -64,3 +64,21 @@ def test_sites_partition():
         for w in (1, 2, 4):
             got = sorted(j for r in range(w) for j in sites_of(r, w, m))
             assert got == list(range(m))
+
+
+@pytest.mark.parametrize("window,latency", [(0, 2), (120, 0), (120, 3)])
+def test_threshold_replay_window_and_latency(orc, window, latency):
+    """The norm-only replay in sliding-window mode (distributed.cpp:33-55:
+    exact window mass, signed deltas, the broadcast replaces the estimate) and
+    with delivery latency (:226-239): thresholds bit-identical to the oracle
+    simulator, broadcasts equal, mass bytes within its total."""
+    from paper_2601_02019_b200.capi import DistProtocol
+    streams = _streams()
+    ref = orc.dist_run(streams, EPS, query_every=0, seed=SEED, want_thetas=True, probes=False,
+                       window=window, latency=latency)
+    p = DistProtocol(M, EPS, latency, window)
+    sq = np.cumsum(streams ** 2, axis=-1)[..., -1]
+    th = np.concatenate([p.advance(sq[:, b:b + 77]) for b in range(0, T, 77)], axis=1)
+    assert np.array_equal(th, ref["thetas"])
+    assert p.info()["broadcasts"] == ref["broadcasts"]
+    assert 0 <= ref["comm_bytes"] - p.info()["mass_bytes"]

@@ -409,6 +409,89 @@ def test_distributed_merge_parity(orc):
     assert np.max(np.abs(np.array(errs) - ref["probe_err"])) <= 1e-6
 
 
+@pytest.mark.parametrize("window,latency", [(150, 0), (150, 2), (0, 2)])
+def test_distributed_window_and_latency_parity(orc, window, latency):
+    """dist-sw (SiteState with a window, distributed.cpp:33-55, 87-97;
+    CoordinatorState window mode, :137-144) and delivery latency (:226-239)
+    through DistributedSketch: per-site thresholds, protocol bytes (FroMass
+    deltas, broadcasts, SnapshotUpdate and Expire messages) exact, probe
+    errors against the windowed exact Gram within 1e-6 of the oracle's."""
+    from paper_2601_02019_b200.distributed import DistributedSketch
+    m, d, eps, T, qe = 4, 32, 0.2, 800, 100
+    streams = np.stack([uniform_rows(orc, T, d, 3, j) for j in range(m)])
+    ref = orc.dist_run(streams, eps, query_every=qe, seed=3, window=window, latency=latency)
+    ds = DistributedSketch(d, eps, m, seed=3, window=window, latency=latency)
+    g = orc.OracleGram(d, window=window)
+    errs = []
+    for b in range(0, T, qe):
+        ds.ingest({j: streams[j, b:b + qe] for j in range(m)}, b + 1)
+        # tick-major like the simulator's oracle.add (distributed.cpp:217-225)
+        g.add_block(streams[:, b:b + qe].transpose(1, 0, 2).reshape(-1, d),
+                    np.repeat(np.arange(b + 1, b + qe + 1), m))
+        sk, gram = ds.probe(want_gram=True)
+        errs.append(g.error(sk))
+    assert ds.exchange.mass_bytes + ds.snapshot_bytes == ref["comm_bytes"]
+    assert ds.exchange.broadcasts == ref["broadcasts"]
+    assert rel_fro(gram, ref["last_probe_gram"]) < 1e-9
+    assert np.max(np.abs(np.array(errs) - ref["probe_err"])) <= 1e-6
+
+
+def _gloo_merge_worker(rank, world, port, outdir):
+    import os as _os
+    import sys as _sys
+    _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from oracle import pyoracle as orc_
+    from paper_2601_02019_b200.distributed import DistributedSketch
+    from refutil import uniform_rows as ur
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, d, eps, T, qe = 4, 32, 0.2, 600, 100
+    streams = np.stack([ur(orc_, T, d, 3, j) for j in range(m)])
+    ds = DistributedSketch(d, eps, m, seed=3, rank=rank, world=world, use_nccl=False)
+    errs, grams = [], []
+    g = orc_.OracleGram(d)
+    for b in range(0, T, qe):
+        ds.ingest({j: streams[j, b:b + qe] for j in ds.exchange.local}, b + 1)
+        for j in range(m):
+            g.add_block(streams[j, b:b + qe], np.arange(b + 1, b + qe + 1))
+        sk, gram = ds.probe(want_gram=True)
+        if rank == 0:
+            errs.append(g.error(sk))
+            grams.append(gram)
+    nbytes = torch.tensor([ds.comm_bytes_local()], dtype=torch.int64)
+    dist.all_reduce(nbytes)
+    if rank == 0:
+        np.save(_os.path.join(outdir, "errs.npy"), np.array(errs))
+        np.save(_os.path.join(outdir, "gram.npy"), grams[-1])
+        np.save(_os.path.join(outdir, "bytes.npy"), np.array([int(nbytes[0]) + ds.exchange.mass_bytes]))
+    dist.destroy_process_group()
+
+
+def test_distributed_merge_across_processes(orc, tmp_path):
+    """World-2 run of DistributedSketch: each process hosts two of the four
+    sites (device sketches on the one GPU), the thresholds come from the
+    norm all-reduce + replay, and the d x d merge crosses the process
+    boundary (gloo reduce of the per-rank Grams, shrink on the root). Probe
+    errors, the last merged Gram and the protocol bytes match the oracle
+    simulator (distributed.cpp:177-269)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gloo_merge_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    m, d, eps, T, qe = 4, 32, 0.2, 600, 100
+    streams = np.stack([uniform_rows(orc, T, d, 3, j) for j in range(m)])
+    ref = orc.dist_run(streams, eps, query_every=qe, seed=3)
+    errs = np.load(tmp_path / "errs.npy")
+    assert np.max(np.abs(errs - ref["probe_err"])) <= 1e-6
+    assert rel_fro(np.load(tmp_path / "gram.npy"), ref["last_probe_gram"]) < 1e-9
+    assert int(np.load(tmp_path / "bytes.npy")[0]) == ref["comm_bytes"]
+
+
 def test_single_site_equals_attp(orc):  # test_distributed.cpp:161-194
     d, eps, T = 8, 0.25, 300
     rows = uniform_rows(orc, T, d, 5, 0)
@@ -737,3 +820,32 @@ def test_amplified_window_bookkeeping(orc):
         assert (q["level"], q["fallback"], q["xi_sum"]) == (qr["level"], qr["fallback"], qr["xi_sum"])
         assert abs(g.error(q["sketch"]) - g.error(qr["sketch"])) <= 1e-6
         assert g.error(q["sketch"]) <= eps
+
+
+# ---------------------------------------------------------------- AdaptiveState
+@pytest.mark.parametrize("dx,dy,eps,theta0,n,T,blk", [(24, 16, 0.25, 0.05, 100, 600, 97),
+                                                      (64, 48, 1 / 8, 0.2, 250, 1200, 256)])
+def test_adaptive_state_matches_oracle(orc, dx, dy, eps, theta0, n, T, blk):
+    """AdaptiveState (amm.cpp:131-161) against the oracle: main's decision
+    trace, the level after every row (threshold doubling / halving with the
+    queue length), the main/aux swap at every window boundary, and the
+    restored product of the main sketch."""
+    xs, ys = orc.gen_amm_rows(5, dx, dy, 4, 0.1, 64.0, 1, T)
+    ref = orc.AdaptiveState(dx, dy, eps, theta0, n, 5, 1000)
+    s = prod.AdaptiveState(dx, dy, eps, theta0, n, seed=5, stream=1000)
+    levels = []
+    for b in range(0, T, blk):
+        ts = np.arange(b + 1, min(b + blk, T) + 1)
+        r = ref.update_block(xs[b:b + blk], ys[b:b + blk], ts)
+        ev, lv = s.update_block(xs[b:b + blk], ys[b:b + blk], ts)
+        assert_trace_equal(ev, r["events"], rtol=1e-7)
+        assert np.array_equal(lv, r["level"]), (b, np.nonzero(lv != r["level"])[0][:5])
+        assert s.info()["theta_main"] == r["theta"][-1]
+        assert s.info()["snaps_main"] == r["nsnaps"][-1]
+        assert rel_fro(s.query_product(), ref.query_product()) < 1e-8
+        levels.append(lv)
+    lv = np.concatenate(levels)
+    assert lv.max() > 1 and np.any(np.diff(lv) < 0), "config must exercise doubling and halving"
+    a, bb = s.query()
+    ar, br = ref.query()
+    assert rel_fro(a @ bb.T, ar @ br.T) < 1e-7
