@@ -38,8 +38,9 @@ CONFIGS = {
                window=65536, drift=131072, rows_per_step=4096, cpu_rows=600,
                name="C3 sliding window N=65536 n=1048576 d=1024 eps=1/64 R=1024 (k=64, drift 131072)"),
     "c4": dict(kind="dist", d=2048, eps=1 / 128, k=128, rho=0.97, noise=0.1, r_max=64.0, n=1048576,
-               k2=16, rho2=0.9, scale2=0.5, rows_per_step=4096, cpu_rows=300,
-               name="C4 distributed, one site per GPU, d=2048 eps=1/128 (global k=128 + site k=16, noise 0.1, R=64)"),
+               k2=16, rho2=0.9, scale2=0.5, rows_per_step=4096, cpu_rows=300, sites=8,
+               name="C4 distributed, m=8 sites spread over the GPUs (one per GPU at 8), d=2048 eps=1/128 "
+                    "(global k=128 + site k=16, noise 0.1, R=64)"),
     "c5": dict(kind="amm", dx=1024, dy=768, d=1024, eps=1 / 64, latent=48, noise=0.1, r_max=64.0,
                n=1048576, window=65536, rows_per_step=512, cpu_rows=200,
                name="C5 sliding-window AMM dx=1024 dy=768 N=65536 eps=1/64 (latent 48, noise 0.1)"),
@@ -52,7 +53,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 (the headline) on one GPU; c4 (the distributed config, "
+                         "m=8 sites over the N GPUs) under torchrun with N > 1")
+    ap.add_argument("--sites", type=int, default=0, help="C4 site count m (default 8, fixed as N grows)")
     ap.add_argument("--rows-per-step", type=int, default=0)
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -267,7 +271,7 @@ def run_reference(args, cfg, rank):
     threads = os.cpu_count() or 1
     orc.set_threads(threads)
     if cfg["kind"] != "attp":
-        sites = args.gpus if cfg["kind"] == "dist" else 1
+        sites = (args.sites or cfg.get("sites", 8)) if cfg["kind"] == "dist" else 1
         n = max(20, (args.cpu_rows or cfg["cpu_rows"]) // sites)
         v, _ = cpu_other_rate(cfg, n, threads, sites=sites)
         unit = "row-site updates/s" if cfg["kind"] == "dist" else "rows/s"
@@ -399,13 +403,12 @@ def run_other(args, cfg, world, rank, local):
                "d2h_bytes_per_step": S * 64}
         extra["value_path"] = "host rows through the public API (CodState has no device-pointer entry point)"
     else:
-        rows = torch.empty((nrows, cfg["d"]), dtype=torch.float64, device=dev)
-        prod.gen_rows_device(rows, 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1,
-                             stream=rank, drift=cfg.get("drift", 0), k2=cfg.get("k2", 0),
-                             rho2=cfg.get("rho2", 0.9), scale2=cfg.get("scale2", 0.5), device=local)
-        torch.cuda.synchronize(dev)
-        host = rows.cpu().pin_memory().numpy()
         if kind == "sw":
+            rows = torch.empty((nrows, cfg["d"]), dtype=torch.float64, device=dev)
+            prod.gen_rows_device(rows, 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1,
+                                 stream=0, drift=cfg.get("drift", 0), device=local)
+            torch.cuda.synchronize(dev)
+            host = rows.cpu().pin_memory().numpy()
             def make():
                 return prod.MlState(cfg["d"], cfg["window"], cfg["r_max"], cfg["eps"], seed=1, stream=1000,
                                     device=local)
@@ -416,23 +419,51 @@ def run_other(args, cfg, world, rank, local):
             ms2, _, _ = timed(lambda sl: st2.update_block(host[sl], ts_all[sl]))
             del st2
             unit_rows = 1
-        else:  # dist: sites j == rank (m = world)
-            from paper_2601_02019_b200.distributed import DistributedSketch
+        else:  # dist: m sites (fixed) spread over the ranks, j % world == rank
+            from paper_2601_02019_b200.distributed import DistributedSketch, sites_of
+            m = args.sites or cfg.get("sites", 8)
+            mine = sites_of(rank, world, m)
+            rows = {}
+            for j in mine:  # site j = data stream j (bench.cpp:240-241)
+                rows[j] = torch.empty((nrows, cfg["d"]), dtype=torch.float64, device=dev)
+                prod.gen_rows_device(rows[j], 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"],
+                                     seed=1, stream=j, k2=cfg.get("k2", 0), rho2=cfg.get("rho2", 0.9),
+                                     scale2=cfg.get("scale2", 0.5), device=local)
+            torch.cuda.synchronize(dev)
+            host = {j: r.cpu().pin_memory().numpy() for j, r in rows.items()}
 
             def make():
-                return DistributedSketch(cfg["d"], cfg["eps"], world, seed=1, rank=rank, world=world,
+                return DistributedSketch(cfg["d"], cfg["eps"], m, seed=1, rank=rank, world=world,
                                          group=group, device=local, use_nccl=world > 1)
             st1 = make()
-            ms, launches, clocks = timed(lambda sl: st1.ingest({rank: rows[sl]}, sl.start + 1))
-            sk, _ = st1.probe()  # NCCL merge (outside the timed region, like the reference's probes)
-            extra["probe_ok"] = bool(np.isfinite(sk).all())
+            ms, launches, clocks = timed(lambda sl: st1.ingest({j: r[sl] for j, r in rows.items()}, sl.start + 1))
+            # merged sketch over NCCL and its covariance error against the pooled
+            # exact Gram of every row all sites ingested (outside the timed region,
+            # like the reference's probes; acceptance.cpp:248-387)
+            sk, _ = st1.probe()
+            gram = torch.zeros((cfg["d"], cfg["d"]), dtype=torch.float64, device=dev)
+            mass = torch.zeros((), dtype=torch.float64, device=dev)
+            for r in rows.values():
+                gram.addmm_(r.T, r)
+                mass += (r * r).sum()
+            if world > 1:
+                torch.distributed.reduce(gram, 0)
+                torch.distributed.reduce(mass, 0)
+            if rank == 0:
+                bt = torch.from_numpy(sk).to(dev)
+                err = torch.linalg.eigvalsh(gram - bt.T @ bt).abs().max() / mass
+                extra["merged_cov_err"] = float(err)
+                extra["merged_cov_err_le_eps"] = bool(float(err) <= cfg["eps"])
+                extra["merged_rows"] = m * nrows
+            extra["comm_bytes_snapshots_rank0"] = st1.comm_bytes_local()
+            extra["mass_protocol_bytes"] = st1.exchange.mass_bytes
             del st1
             st2 = make()
-            ms2, _, _ = timed(lambda sl: st2.ingest({rank: host[sl]}, sl.start + 1))
+            ms2, _, _ = timed(lambda sl: st2.ingest({j: h[sl] for j, h in host.items()}, sl.start + 1))
             del st2
-            unit_rows = world
+            unit_rows = m
         e2e = {"value": unit_rows * S * steps / (ms2 * 1e-3), "unit": "row-site updates/s" if kind == "dist" else "rows/s",
-               "h2d_bytes_per_step": S * cfg["d"] * 8, "d2h_bytes_per_step": 0}
+               "h2d_bytes_per_step": S * cfg["d"] * 8 * (len(rows) if kind == "dist" else 1), "d2h_bytes_per_step": 0}
     value = unit_rows * S * steps / (ms * 1e-3)
     if rank == 0:
         cpu = None
@@ -444,9 +475,11 @@ def run_other(args, cfg, world, rank, local):
             "metric": "sketch update throughput", "value": value,
             "unit": "row-site updates/s" if kind == "dist" else "rows/s", "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if kind == "dist" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": cfg["name"], "rows_per_step": S, "timed_rows": f"{warm * S + 1}..{nrows}",
-                       "parallelism": f"sites={world}" if kind == "dist" else "single"},
+                       "parallelism": (f"sites={unit_rows} over {world} GPU(s) ({unit_rows // world} per GPU), "
+                                       f"ncclReduce merge") if kind == "dist" else "single"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, **extra}), flush=True)
     if world > 1:
@@ -455,8 +488,10 @@ def run_other(args, cfg, world, rank, local):
 
 def main():
     args = parse()
-    cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:  # north_star: 1 GPU for the persistent configs, 1-8 for the distributed one
+        args.config = "c4" if max(world, args.gpus) > 1 else "c2"
+    cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

@@ -152,23 +152,49 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, double alpha,
 // ingestion (K1): per-row squared norm + finiteness, one warp per row,
 // coalesced 8-byte loads (reference sketch.cpp:83-84, attp.hpp:22)
 // ============================================================================
-__global__ void k_ingest(const double* __restrict__ rows, int64_t n, int64_t ld, int d,
-                         double* __restrict__ nrm2, int* __restrict__ bad) {
+// K1 (ingestion, sketch.cpp:83-85 + attp.hpp:22): squared norm and
+// finiteness of each row, one warp per row. VEC: 16-byte loads (rows 16-byte
+// aligned, d even) with four independent accumulators so every lane keeps 4
+// loads in flight; the per-row sum order is fixed (deterministic).
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_ingest(const double* __restrict__ rows, int64_t n, int64_t ld, int d,
+                                                double* __restrict__ nrm2, int* __restrict__ bad) {
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const double* a = rows + row * ld;
-    double s = 0.0;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
     int nf = 0;
-    for (int j = lane; j < d; j += 32) {
-        const double v = a[j];
-        nf |= !isfinite(v);
-        s = fma(v, v, s);
+    if (VEC) {
+        const double2* a2 = reinterpret_cast<const double2*>(a);
+        const int d2 = d >> 1;
+        int j = lane;
+        for (; j + 96 < d2; j += 128) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(a2 + j + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                nf |= !isfinite(v[u].x) | !isfinite(v[u].y);
+                s[u] = fma(v[u].y, v[u].y, fma(v[u].x, v[u].x, s[u]));
+            }
+        }
+        for (; j < d2; j += 32) {
+            const double2 v = __ldcs(a2 + j);
+            nf |= !isfinite(v.x) | !isfinite(v.y);
+            s[0] = fma(v.y, v.y, fma(v.x, v.x, s[0]));
+        }
+    } else {
+        for (int j = lane; j < d; j += 32) {
+            const double v = a[j];
+            nf |= !isfinite(v);
+            s[0] = fma(v, v, s[0]);
+        }
     }
-    s = warp_sum(s);
+    double t = warp_sum((s[0] + s[1]) + (s[2] + s[3]));
     nf = __any_sync(0xffffffffu, nf);
     if (lane == 0) {
-        nrm2[row] = s;
+        nrm2[row] = t;
         bad[row] = nf;
     }
 }
@@ -176,7 +202,11 @@ void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int
                  int* bad) {
     if (n <= 0) return;
     const int wpb = 8;
-    k_ingest<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(rows, n, ld, d, nrm2, bad);
+    const bool vec = !(d & 1) && !(ld & 1) && !((uintptr_t)rows & 15);
+    if (vec)
+        k_ingest<true><<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(rows, n, ld, d, nrm2, bad);
+    else
+        k_ingest<false><<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, st>>>(rows, n, ld, d, nrm2, bad);
     AERO_LAUNCHED();
 }
 

@@ -48,6 +48,10 @@ struct OzakiGram {
     void product(cudaStream_t st, int N, const double* X, int ldx, const int* colmask, double* Y, int ldy,
                  double* ws, size_t ws_doubles);
     void reserve_x(int N);  // X slice buffers for N columns
+    // allocate the slice buffers for up to Rmax rows and Nmax columns once
+    // (growing them on demand costs a cudaFree -- a device-wide sync -- plus a
+    // cudaMalloc inside the update loop)
+    void reserve(int Rmax, int Nmax);
     void release();
     ~OzakiGram() { release(); }
 };

@@ -126,6 +126,32 @@ void OzakiGram::prepare(cudaStream_t st, int R_, const double* G, int ldg) {
     AERO_LAUNCHED();
 }
 
+void OzakiGram::reserve(int Rmax, int Nmax) {
+    const int Rp_ = (Rmax + OZ_BM - 1) / OZ_BM * OZ_BM, Kp_ = (Rmax + OZ_BK - 1) / OZ_BK * OZ_BK;
+    const int Np = (Nmax + OZ_BN - 1) / OZ_BN * OZ_BN;
+    const size_t na = (size_t)kSlices * Rp_ * Kp_, nb = (size_t)kSlices * Np * Kp_;
+    if (a_bytes < na) {
+        if (a) cudaFree(a);
+        AERO_CUDA(cudaMalloc(&a, na));
+        a_bytes = na;
+    }
+    if (ea_n < (size_t)Rp_) {
+        if (ea) cudaFree(ea);
+        AERO_CUDA(cudaMalloc(&ea, sizeof(int) * Rp_));
+        ea_n = Rp_;
+    }
+    if (b_bytes < nb) {
+        if (b) cudaFree(b);
+        AERO_CUDA(cudaMalloc(&b, nb));
+        b_bytes = nb;
+    }
+    if (fb_n < (size_t)Np) {
+        if (fb) cudaFree(fb);
+        AERO_CUDA(cudaMalloc(&fb, sizeof(int) * Np));
+        fb_n = Np;
+    }
+}
+
 void OzakiGram::reserve_x(int N) {
     const int Np = (N + OZ_BN - 1) / OZ_BN * OZ_BN;
     const size_t need = (size_t)kSlices * Np * Kp;

@@ -116,6 +116,7 @@ Sketch::Sketch(const aero_cfg& cfg) {
     sig_.alloc(ncols_);
     vr_.alloc((size_t)ncols_ * kv_);
     small_.alloc(4 * 64 * 64 + 64);
+    if (i8_ && cap_ >= i8_min_rows_) oz_.reserve(cap_, ncols_);
     status_d_ = dev_alloc<int>(ncols_);
     clamp_d_ = dev_alloc<int>(ncols_);
     colmask_d_ = dev_alloc<int>(ncols_);
@@ -129,10 +130,15 @@ Sketch::Sketch(const aero_cfg& cfg) {
     status_h_ = pinned<int>(ncols_);
     clamp_h_ = pinned<int>(ncols_);
     stage_rows_ = 4096;
-    nrm_.alloc(stage_rows_);
-    bad_d_ = dev_alloc<int>(stage_rows_);
-    nrm_h_ = pinned<double>(stage_rows_);
-    bad_h_ = pinned<int>(stage_rows_);
+    nrm_.alloc(2 * (size_t)stage_rows_);
+    bad_d_ = dev_alloc<int>(2 * (size_t)stage_rows_);
+    nrm_h_ = pinned<double>(2 * (size_t)stage_rows_);
+    bad_h_ = pinned<int>(2 * (size_t)stage_rows_);
+    AERO_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        AERO_CUDA(cudaEventCreateWithFlags(&ev_ready_[b], cudaEventDisableTiming));
+        AERO_CUDA(cudaEventCreateWithFlags(&ev_free_[b], cudaEventDisableTiming));
+    }
 }
 
 cudaEvent_t Sketch::ev_at(size_t i) {
@@ -164,6 +170,14 @@ Sketch::~Sketch() {
     cudaFree(colmask_d_);
     cudaFree(jobs_d_);
     cudaFree(bad_d_);
+    if (cs_) {
+        cudaStreamSynchronize(cs_);
+        cudaStreamDestroy(cs_);
+    }
+    for (int b = 0; b < 2; ++b) {
+        if (ev_ready_[b]) cudaEventDestroy(ev_ready_[b]);
+        if (ev_free_[b]) cudaEventDestroy(ev_free_[b]);
+    }
     cudaFreeHost(jobs_h_);
     cudaFreeHost(colmask_h_);
     cudaFreeHost(sig_h_);
@@ -692,7 +706,12 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
     // firing regime ends one batch, not two)
     // (amplified rows finish every fired gate exactly: r candidates + scoring)
     const Pattern pat = (!amp_ && fire_ema_ >= 0.5) ? FIRE1 : NOFIRE;
+    const auto pa = std::chrono::steady_clock::now();
     append_rows(dev_rows, B);
+    if (host_prof_) {
+        AERO_CUDA(cudaStreamSynchronize(st_));
+        prof_append_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pa).count();
+    }
     const int R = r0 + (int)B;
     int njobs = 0;
     const int gate_base = (pat == FIRE1) ? 2 * (int)B : 0;
@@ -711,7 +730,10 @@ int64_t Sketch::run_batch(const double* dev_rows, int64_t B, const int64_t* t,
         jobs_h_[njobs++] = IterJob{0, rj, 1, gate_base + j, kp_ + 1, -1, fork_state0(gf), gf};
         colmask_h_[gate_base + j] = rj;
     }
+    const auto pi = std::chrono::steady_clock::now();
     run_iterate(njobs, R, 2);
+    if (host_prof_)
+        prof_iter_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pi).count();
     batches++;
     const int simul_job0 = 0, gate_job0 = (pat == FIRE1) ? (int)B : 0;
     uint64_t forks = F;
@@ -827,7 +849,12 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
             ev->t = t[pos];
             ev->theta = thetas[pos];
             theta_ = thetas[pos];
+            const auto s0 = std::chrono::steady_clock::now();
             single_row(dev_rows + (size_t)pos * d_, t[pos], thetas[pos], ev);
+            if (host_prof_) {
+                const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
+                if (ms > 40.0) fprintf(stderr, "  slow single_row t=%lld r=%d reduce=%d: %.1f ms\n", (long long)t[pos], r_, ev->reduced, ms);
+            }
             fire_ema_ = 0.95 * fire_ema_ + 0.05 * (ev->gate_fired ? 1.0 : 0.0);
             rows_processed++;
             pos++;
@@ -842,7 +869,12 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
         cur_batch_ = (int)std::clamp(std::sqrt(two_alpha / p), 16.0, (double)max_batch_);
         const int64_t B = std::min<int64_t>({(int64_t)cur_batch_, n - pos, room});
         const int64_t mp0 = mispredicts;
+        const auto b0 = std::chrono::steady_clock::now();
         const int64_t used = run_batch(dev_rows + (size_t)pos * d_, B, t + pos, thetas + pos, log + pos);
+        if (host_prof_) {
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - b0).count();
+            if (ms > 40.0) fprintf(stderr, "  slow batch t=%lld B=%lld used=%lld r=%d: %.1f ms (append %.1f iterate %.1f)\n", (long long)t[pos], (long long)B, (long long)used, r_, ms, prof_append_ms_, prof_iter_ms_);
+        }
         const double ended = (mispredicts > mp0) ? 1.0 : 0.0;
         const double w = std::min(1.0, (double)used / 256.0);  // EMA over ~256 rows
         end_rate_ = (1.0 - w) * end_rate_ + w * (ended / (double)used);
@@ -865,26 +897,52 @@ void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld
         local.resize(n);
         log = local.data();
     }
+    // Chunks of stage_rows_ rows through two staging buffers: the H2D copy
+    // (pinned host rows: DMA) and the K1 norm/finiteness pass of chunk k+1 run
+    // on the staging stream while chunk k is processed. Device rows with
+    // ld == d are read in place (no staging copy).
+    const int64_t nchunks = (n + stage_rows_ - 1) / stage_rows_;
+    const bool in_place = device && ld == d_;
+    const double* src[2] = {nullptr, nullptr};
+    auto prefetch = [&](int64_t k) {
+        const int b = (int)(k & 1);
+        const int64_t off = k * stage_rows_, cnt = std::min<int64_t>(stage_rows_, n - off);
+        if (in_place) {
+            src[b] = rows + off * ld;
+            AERO_CUDA(cudaStreamWaitEvent(cs_, ev_free_[b], 0));
+        } else {
+            stage_[b].alloc((size_t)stage_rows_ * d_);
+            AERO_CUDA(cudaStreamWaitEvent(cs_, ev_free_[b], 0));  // chunk k-2 is done with it
+            AERO_CUDA(cudaMemcpy2DAsync(stage_[b].p, sizeof(double) * d_, rows + off * ld, sizeof(double) * ld,
+                                        sizeof(double) * d_, cnt,
+                                        device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, cs_));
+            src[b] = stage_[b].p;
+        }
+        double* nd = nrm_.p + (size_t)b * stage_rows_;
+        int* bd = bad_d_ + (size_t)b * stage_rows_;
+        ingest_rows(cs_, src[b], cnt, d_, d_, nd, bd);
+        AERO_CUDA(cudaMemcpyAsync(nrm_h_ + (size_t)b * stage_rows_, nd, sizeof(double) * cnt, cudaMemcpyDeviceToHost, cs_));
+        AERO_CUDA(cudaMemcpyAsync(bad_h_ + (size_t)b * stage_rows_, bd, sizeof(int) * cnt, cudaMemcpyDeviceToHost, cs_));
+        AERO_CUDA(cudaEventRecord(ev_ready_[b], cs_));
+    };
+    // events start "free": record them once on the sketch stream
+    for (int b = 0; b < 2; ++b) AERO_CUDA(cudaEventRecord(ev_free_[b], st_));
     std::vector<double> th;
-    for (int64_t off = 0; off < n; off += stage_rows_) {
-        const int64_t cnt = std::min<int64_t>(stage_rows_, n - off);
-        stage_.alloc((size_t)stage_rows_ * d_);
-        // stage rows contiguously (ld = d) on the device
-        AERO_CUDA(cudaMemcpy2DAsync(stage_.p, sizeof(double) * d_, rows + off * ld,
-                                    sizeof(double) * ld, sizeof(double) * d_, cnt,
-                                    device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                    st_));
-        ingest_rows(st_, stage_.p, cnt, d_, d_, nrm_.p, bad_d_);
-        AERO_CUDA(cudaMemcpyAsync(nrm_h_, nrm_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
-        AERO_CUDA(cudaMemcpyAsync(bad_h_, bad_d_, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st_));
-        AERO_CUDA(cudaStreamSynchronize(st_));
+    prefetch(0);
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int b = (int)(k & 1);
+        const int64_t off = k * stage_rows_, cnt = std::min<int64_t>(stage_rows_, n - off);
+        if (k + 1 < nchunks) prefetch(k + 1);
+        AERO_CUDA(cudaEventSynchronize(ev_ready_[b]));
+        const double* nrm_h = nrm_h_ + (size_t)b * stage_rows_;
+        const int* bad_h = bad_h_ + (size_t)b * stage_rows_;
         // validation in row order (sketch.cpp:83-85): the first offending row
         // raises after the rows before it were absorbed
         int64_t good = cnt;
         std::string err;
         int64_t prev = (off == 0) ? clock_ : t[off - 1];
         for (int64_t j = 0; j < cnt; ++j) {
-            if (bad_h_[j]) { good = j; err = "AeroState: non-finite row"; break; }
+            if (bad_h[j]) { good = j; err = "AeroState: non-finite row"; break; }
             if (t[off + j] <= prev) { good = j; err = "AeroState: timestamp regression"; break; }
             if (mode_ != AERO_THETA_ATTP && theta_per_row && theta_per_row[off + j] < 0.0) {
                 good = j;  // set_theta throws before this row's update (sketch.cpp:33-36)
@@ -896,7 +954,7 @@ void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld
         th.resize(good);
         for (int64_t j = 0; j < good; ++j) {
             if (mode_ == AERO_THETA_ATTP) {  // attp.hpp:22-23
-                fro_mass_ += nrm_h_[j];
+                fro_mass_ += nrm_h[j];
                 th[j] = eps_ * fro_mass_;
             } else if (theta_per_row) {
                 th[j] = theta_per_row[off + j];
@@ -904,9 +962,20 @@ void Sketch::update_block(const double* rows, bool device, int64_t n, int64_t ld
                 th[j] = theta_;
             }
         }
-        process_rows(stage_.p, good, t + off, th.data(), log + off);
-        if (good < cnt) throw InvalidInput(err);
+        AERO_CUDA(cudaStreamWaitEvent(st_, ev_ready_[b], 0));
+        try {
+            process_rows(src[b], good, t + off, th.data(), log + off);
+        } catch (...) {
+            cudaStreamSynchronize(cs_);  // no DMA from the caller's rows after we return
+            throw;
+        }
+        AERO_CUDA(cudaEventRecord(ev_free_[b], st_));
+        if (good < cnt) {
+            AERO_CUDA(cudaStreamSynchronize(cs_));
+            throw InvalidInput(err);
+        }
     }
+    AERO_CUDA(cudaStreamSynchronize(cs_));
 }
 
 // ---------------------------------------------------------------- queries

@@ -133,6 +133,8 @@ class Sketch {
     cudaStream_t st_ = nullptr;
     // host state
     double theta_, fro_mass_ = 0.0;
+    bool host_prof_ = getenv("AERO_HOST_PROF") != nullptr;  // dev instrumentation
+    double prof_append_ms_ = 0.0, prof_iter_ms_ = 0.0;
     int64_t clock_ = 0, last_dump_t_ = 0;
     uint64_t forks_ = 0;
     int r_ = 0;
@@ -143,7 +145,7 @@ class Sketch {
     std::deque<Chunk*> chunks_;
     aero_event last_ev_{};
     // device buffers
-    DeviceBuf C_, C2_, G_, E_, ew_, fw_, stage_, nrm_, X_, Y_, H_, sig_, vr_, small_, Bq_, Wq_,
+    DeviceBuf C_, C2_, G_, E_, ew_, fw_, stage_[2], nrm_, X_, Y_, H_, sig_, vr_, small_, Bq_, Wq_,
         qw_, qy_, ws_;
     static constexpr int kMaxPhases = 256;
     int* phase_d_ = nullptr;   // per-phase active columns | split-K factors (persistent iterate)
@@ -167,7 +169,9 @@ class Sketch {
     int* status_d_ = nullptr;
     int* clamp_d_ = nullptr;
     int* colmask_d_ = nullptr;
-    int* bad_d_ = nullptr;
+    int* bad_d_ = nullptr;  // 2 x stage_rows_ (one half per staging buffer)
+    cudaStream_t cs_ = nullptr;  // staging stream: H2D + K1 of chunk k+1 overlap chunk k
+    cudaEvent_t ev_ready_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
     IterJob* jobs_d_ = nullptr;
     int ldx_ = 0, ncols_ = 0, kv_ = 64, stage_rows_ = 0;
     // pinned host mirrors

@@ -542,6 +542,214 @@ size_t sytrd_cluster_smem(int n, int cs) {
     return sizeof(double) * ((size_t)cw * n + 5 * (size_t)n + 2 * (cs + 4) + 64);
 }
 
+// n in (512, 2048]: unblocked dsytd2 (same arithmetic as k_sytrd_small) with
+// the matrix RESIDENT IN SHARED MEMORY, distributed by rows: CTA q owns rows
+// q, q + G, q + 2G, ... (cyclic, so every CTA keeps work until the end; at
+// n = 2048 and G = 148 that is 14 full rows = 224 KiB). Every vector indexed by
+// the column (x = the column being reduced, v, w) lives in registers of the
+// thread owning that column index (cc = tid + SR_NT m), identically in every
+// CTA, so per column there is ONE grid barrier and no other global round trip:
+//   1. reflector v_j from x_j: block reduction of |x|^2, redundant per CTA
+//   2. ONE fused pass over the own rows: apply the pending rank-2 update of
+//      reflector j-1 (A -= v w^T + w v^T) and accumulate y = A v_j
+//   3. publish y (own rows) and row j+1 (the next column, updates <= j-1);
+//      -- grid barrier --
+//   4. every CTA loads y and row j+1 (one L2 round), w = tau y,
+//      alpha = -tau/2 w.v, w += alpha v, and x_{j+1} = row j+1 - v w_{j+1} - w v_{j+1}
+// y and the next column are double-buffered by column parity: a CTA can only
+// overwrite a buffer after every CTA passed the barrier that follows its reads.
+constexpr int SR_NT = 512;  // threads per CTA
+constexpr int SR_M = 4;     // column indices per thread (n <= SR_NT * SR_M)
+constexpr int SR_R = 14;    // rows per CTA (smem: 14 x 2048 doubles)
+constexpr int SR_NW = SR_NT / 32;
+constexpr int kSytrdRowsMax = SR_NT * SR_M;
+
+size_t sytrd_rows_smem(int n, int R) { return sizeof(double) * ((size_t)R * n + SR_NW * 16 + 2 * SR_R + 8); }
+
+struct SrArgs {
+    int n, lda, R;
+    const double* A;  // n x n symmetric (both triangles), column-major
+    double *V, *d, *e, *tau;
+    double *ypub, *cpub;  // 2 x n each
+    unsigned* bar;
+};
+
+// sum of 16 per-thread values over a warp by recursive halving (16 shuffles
+// instead of 80): returns the total of value idx(lane) (lanes 2i, 2i+1 hold it)
+__device__ __forceinline__ double warp_sum16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const bool up = lane & 16;
+        const double send = up ? v[i] : v[i + 8];
+        const double keep = up ? v[i + 8] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool up = lane & 8;
+        const double send = up ? v[i] : v[i + 4];
+        const double keep = up ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const bool up = lane & 4;
+        const double send = up ? v[i] : v[i + 2];
+        const double keep = up ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {
+        const bool up = lane & 2;
+        const double send = up ? v[0] : v[1];
+        const double keep = up ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+__device__ __forceinline__ int warp_sum16_index(int lane) {
+    return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+__global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int n = a.n, G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int R = a.R;
+    const int nr = (n - cta + G - 1) / G;  // own rows r_k = cta + G k, k < nr (<= R)
+    double* As = sm;                        // nr x n, row k at As + k n
+    double* red = sm + (size_t)R * n;       // SR_NW x 16
+    double* rv = red + SR_NW * 16;          // v_{j-1}(r_k)
+    double* rw = rv + SR_R;                 // w_{j-1}(r_k)
+    double* bc = rw + SR_R;                 // broadcast scalars
+    for (int k = 0; k < nr; ++k) {
+        const double* src = a.A + (int64_t)(cta + G * k) * a.lda;  // row r = column r (symmetric)
+        for (int cc = tid; cc < n; cc += SR_NT) As[(size_t)k * n + cc] = src[cc];
+    }
+    if (tid < SR_R) rv[tid] = rw[tid] = 0.0;
+    double xr[SR_M], vr[SR_M], wr[SR_M];
+#pragma unroll
+    for (int m = 0; m < SR_M; ++m) {
+        const int cc = tid + SR_NT * m;
+        xr[m] = (cc < n) ? a.A[cc] : 0.0;  // column 0
+        vr[m] = wr[m] = 0.0;
+    }
+    unsigned epoch = 0;
+    for (int j = 0; j < n - 1; ++j) {
+        // ---- 1. reflector (dlarfg) from x_j, rows j+1 ..
+        double s2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            const int cc = tid + SR_NT * m;
+            if (cc >= j + 2 && cc < n) s2 = fma(xr[m], xr[m], s2);
+            if (cc == j) bc[0] = xr[m];
+            if (cc == j + 1) bc[1] = xr[m];
+        }
+        s2 = block_sum_d(s2, red);  // syncs: bc visible
+        const double dj = bc[0], alpha = bc[1];
+        double tj = 0.0, beta = alpha, scal = 0.0;
+        if (s2 > 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+            tj = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        double vn[SR_M];
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            const int cc = tid + SR_NT * m;
+            const double vv = (cc == j + 1) ? 1.0 : (cc >= j + 2 && cc < n) ? xr[m] * scal : 0.0;
+            if (cta == 0 && cc > j && cc < n) a.V[cc + (int64_t)j * n] = vv;
+            vn[m] = (tj != 0.0) ? vv : 0.0;
+        }
+        if (cta == 0 && tid == 0) {
+            a.d[j] = dj;
+            a.e[j] = beta;
+            a.tau[j] = tj;
+        }
+        // ---- 2. fused pass: pending update j-1, then y = A v_j (own rows >= j+1)
+        const int k0 = (j + 1 <= cta) ? 0 : (j + 1 - cta + G - 1) / G;  // first own row >= j+1
+        double acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            const int cc = tid + SR_NT * m;
+            if (cc >= j + 1 && cc < n) {
+                const double vo = vr[m], wo = wr[m], vj = vn[m];
+#pragma unroll
+                for (int k = 0; k < SR_R; ++k) {
+                    if (k >= k0 && k < nr) {
+                        double* p = As + (size_t)k * n + cc;
+                        const double x = fma(-rw[k], vo, fma(-rv[k], wo, *p));
+                        *p = x;
+                        acc[k] = fma(x, vj, acc[k]);
+                    }
+                }
+            }
+        }
+        // row j+1 after updates <= j-1 is the next column (symmetry): publish it
+        double* cpub = a.cpub + (size_t)(j & 1) * n;
+        double* ypub = a.ypub + (size_t)(j & 1) * n;
+        if ((j + 1) % G == cta) {
+            const int k1 = (j + 1) / G;
+#pragma unroll
+            for (int m = 0; m < SR_M; ++m) {
+                const int cc = tid + SR_NT * m;
+                if (cc >= j + 1 && cc < n) __stcg(cpub + cc, As[(size_t)k1 * n + cc]);
+            }
+        }
+        // ---- 3. y(r_k) = block sum of acc[k], publish
+        {
+            const double ws = warp_sum16(acc, lane);
+            const int idx = warp_sum16_index(lane);
+            __syncthreads();  // red: the reflector's block sum is read by now
+            if (!(lane & 1)) red[warp * 16 + idx] = ws;
+            __syncthreads();
+            if (tid < nr && tid >= k0) {
+                double y = 0.0;
+                for (int w = 0; w < SR_NW; ++w) y += red[w * 16 + tid];
+                __stcg(ypub + cta + G * tid, y);
+            }
+        }
+        grid_sync(a.bar, epoch, G);
+        // ---- 4. w = tau y; alpha = -tau/2 w.v; w += alpha v; next column
+        double yv[SR_M], cv[SR_M];
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            const int cc = tid + SR_NT * m;
+            const bool act = cc >= j + 1 && cc < n;
+            yv[m] = act ? __ldcg(ypub + cc) : 0.0;
+            cv[m] = act ? __ldcg(cpub + cc) : 0.0;
+        }
+        double dot = 0.0;
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            yv[m] *= tj;
+            dot = fma(yv[m], vn[m], dot);
+            if (tid + SR_NT * m == j + 1) bc[2] = yv[m];
+        }
+        dot = block_sum_d(dot, red);
+        const double al = -0.5 * tj * dot;
+        const double vj1 = (tj != 0.0) ? 1.0 : 0.0;
+        const double wj1 = bc[2] + al * vj1;
+#pragma unroll
+        for (int m = 0; m < SR_M; ++m) {
+            const int cc = tid + SR_NT * m;
+            const double wn = fma(al, vn[m], yv[m]);
+            xr[m] = (cc >= j + 1 && cc < n) ? fma(-wn, vj1, fma(-vn[m], wj1, cv[m])) : 0.0;
+            vr[m] = vn[m];
+            wr[m] = wn;
+            if (cc < n && cc % G == cta) {  // own rows: the pending update's row factors
+                rv[cc / G] = vn[m];
+                rw[cc / G] = wn;
+            }
+        }
+    }
+    // x_{n-1}(n-1): the last diagonal element
+#pragma unroll
+    for (int m = 0; m < SR_M; ++m)
+        if (cta == 0 && tid + SR_NT * m == n - 1) a.d[n - 1] = xr[m];
+}
+
 // Small n (<= kSytrdSmall): unblocked dsytd2 by ONE CTA with the whole matrix
 // in shared memory (no grid barriers). Same outputs as k_sytrd.
 constexpr int kSytrdSmall = 128;
@@ -1147,7 +1355,7 @@ __global__ void k_backtransform_small(int n, int nvec, const double* __restrict_
 }
 
 struct Work {
-    DeviceBuf V, W, vec, Z, Dp, L, Y, S, T, M1, M2, ws;
+    DeviceBuf V, W, vec, Z, Dp, L, Y, S, T, M1, M2, ws, pub;
     unsigned* bar = nullptr;
     int grid = 0;
 };
@@ -1184,6 +1392,8 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sytrd_cluster_smem(kSytrdClusterMax, 16)));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sytrd_rows_smem(kSytrdRowsMax, SR_R)));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * (kSytrdSmall * kSytrdSmall + 2 * kSytrdSmall + 64))));
         AERO_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1234,6 +1444,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     TrdArgs ta{n, lda, A, wk.V.p, wk.W.p, d, e, tau, ybuf, wpre, y0, slots, dots, wk.bar, prof};
     void* args[] = {&ta};
     const bool vec = !(lda & 1) && !((uintptr_t)A & 15);
+    static const bool no_rows = getenv("AERO_SYTRD_ROWS") && atoi(getenv("AERO_SYTRD_ROWS")) == 0;  // dev A/B
     note_launch();
     if (n <= kSytrdSmall) {
         k_sytrd_small<<<1, n <= 64 ? 128 : 512, sizeof(double) * ((size_t)n * n + 2 * n + 64), st>>>(n, A, lda, wk.V.p,
@@ -1271,6 +1482,14 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
                     n, cs, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3);
             cudaFree(cprof);
         }
+    } else if (n <= kSytrdRowsMax && (n + wk.grid - 1) / wk.grid <= SR_R && !no_rows) {
+        // matrix resident in shared memory, one grid barrier per column
+        const int Gr = wk.grid, R = (n + Gr - 1) / Gr;
+        wk.pub.alloc((size_t)4 * n);
+        SrArgs sa{n, lda, R, A, wk.V.p, d, e, tau, wk.pub.p, wk.pub.p + 2 * (size_t)n, wk.bar};
+        void* sargs[] = {&sa};
+        AERO_CUDA(cudaLaunchCooperativeKernel((void*)k_sytrd_rows, dim3(Gr), dim3(SR_NT), sargs,
+                                              sytrd_rows_smem(n, R), st));
     } else {
         AERO_CUDA(cudaLaunchCooperativeKernel(vec ? (void*)k_sytrd<true> : (void*)k_sytrd<false>, dim3(G),
                                               dim3(TRD_THREADS), args, smem, st));

@@ -97,6 +97,7 @@ class DistributedSketch:
         self.coord = Coordinator(d, m, device, self._comm, window=self.window, latency=latency)
         self.snapshot_bytes = 0
         self.clock = 0
+        self._pool = None
 
     def _nccl_comm(self, group):
         import torch
@@ -114,17 +115,33 @@ class DistributedSketch:
         """Feed ticks t0 .. t0+T-1 to the local sites (rows: (T, d) host arrays
         or CUDA float64 tensors)."""
         norms = {}
+        rows_by_site = dict(rows_by_site)
         for j, rows in rows_by_site.items():
-            if hasattr(rows, "is_cuda") and rows.is_cuda:
-                norms[j] = row_sq_norms_device(rows, self.device)
-            else:
-                r = np.asarray(rows, np.float64)
-                norms[j] = np.cumsum(r * r, axis=1)[:, -1]  # sequential, like the reference
+            if not (hasattr(rows, "is_cuda") and rows.is_cuda):
+                # host rows: one H2D (asynchronous from pinned memory), then the
+                # same device path -- norms by the ingestion kernel (K1)
+                import torch
+                t = torch.from_numpy(np.ascontiguousarray(rows, np.float64))
+                rows_by_site[j] = t.to(torch.device("cuda", self.device), non_blocking=t.is_pinned())
+            norms[j] = row_sq_norms_device(rows_by_site[j], self.device)
         theta = self.exchange.thresholds(norms)
         T = theta.shape[1]
         ts = np.arange(t0, t0 + T, dtype=np.int64)
-        for j, rows in rows_by_site.items():
-            self.sites[j].update_block(rows, ts, thetas=theta[j])
+        items = list(rows_by_site.items())
+        if len(items) > 1:
+            # several sites on this GPU: each is its own device state and
+            # stream, so their update blocks run concurrently (the C-ABI call
+            # releases the GIL); absorbs stay serial (one accumulator)
+            if self._pool is None:
+                from concurrent.futures import ThreadPoolExecutor
+                self._pool = ThreadPoolExecutor(max_workers=len(self.sites))
+            futs = [self._pool.submit(self.sites[j].update_block, rows, ts, thetas=theta[j]) for j, rows in items]
+            for f in futs:
+                f.result()
+        else:
+            for j, rows in items:
+                self.sites[j].update_block(rows, ts, thetas=theta[j])
+        for j, _ in items:
             self.snapshot_bytes += self.coord.absorb(self.sites[j])
         self.clock = t0 + T - 1
 

@@ -119,6 +119,36 @@ def test_block_stops_at_first_bad_row():
     assert s.clock == 3  # rows before the offending one were absorbed
 
 
+@pytest.mark.parametrize("where", ["host", "device", "device_strided"])
+def test_multichunk_block_matches_oracle_and_stops_at_bad_row(orc, where):
+    """A 10000-row block crosses the 4096-row staging chunks (double-buffered:
+    the H2D copy and norm pass of chunk k+1 overlap chunk k); host rows,
+    device rows read in place (ld == d) and strided device rows must give the
+    oracle's trace, and a non-finite row in the third chunk stops the block
+    after the rows before it (sketch.cpp:83-85)."""
+    d, n, bad = 16, 10000, 9000
+    rows = orc.gen_rows(d, 4, 0.9, 0.1, 64.0, 3, 0, 1, n)
+    ts = np.arange(1, n + 1)
+    ref = orc.AttpState(d, 0.25, 3, 1000)
+    ev_ref = ref.update_block(rows[:bad], ts[:bad])
+    s = prod.AttpState(d, 0.25, seed=3, stream=1000)
+    blk = rows.copy()
+    blk[bad, 5] = np.nan
+    if where == "host":
+        arg = blk
+    else:
+        t = torch.zeros((n, d + (8 if where == "device_strided" else 0)), dtype=torch.float64, device="cuda")
+        t[:, :d] = torch.from_numpy(blk).cuda()
+        arg = t[:, :d]
+    with pytest.raises(prod.InvalidInput):
+        s.update_block(arg, ts)
+    assert s.clock == bad
+    s2 = prod.AttpState(d, 0.25, seed=3, stream=1000)
+    ev = s2.update_block(rows[:bad] if where == "host" else torch.from_numpy(rows[:bad]).cuda(), ts[:bad])
+    assert_trace_equal(ev, ev_ref)
+    assert rel_fro(s.query_gram(0, bad), ref.inner.query_gram(0, bad)) < 1e-9
+
+
 @pytest.mark.parametrize("exact", [False, True])
 def test_snapshot_invariants_and_trace(orc, exact):  # test_sketch.cpp:178-204
     rows = np.stack([gaussian_vec(orc, 8, 300, i) for i in range(1, 201)])
@@ -328,7 +358,7 @@ def test_ml_bookkeeping_bit_exact(orc, n_win, scale_rows):
 
 
 # ---------------------------------------------------------------- eigensolver
-@pytest.mark.parametrize("n", [2, 7, 32, 64, 96, 97, 128, 256, 301, 512, 1024])
+@pytest.mark.parametrize("n", [2, 7, 32, 64, 96, 97, 128, 256, 301, 512, 513, 777, 1024, 1536, 2048])
 def test_eigh_matches_oracle(orc, n):
     a = gaussian(orc, n + 3, n, 11, n)
     b = a.T @ a
@@ -347,7 +377,7 @@ def test_eigh_matches_oracle(orc, n):
     assert np.max(np.abs(v[:, sep] - vr[:, sep])) < 1e-8
 
 
-@pytest.mark.parametrize("n", [64, 200, 512])
+@pytest.mark.parametrize("n", [64, 200, 512, 700, 2048])
 def test_eigh_repeated_eigenvalues(orc, n):
     """Exactly repeated eigenvalues in a non-axis basis (the tridiagonal form then
     splits or holds numerically equal eigenvalues): eigenvectors must still form
