@@ -276,6 +276,25 @@ int aero_adaptive_query_product(aero_adaptive* h, double* p_dx_by_dy);
 int aero_adaptive_info(aero_adaptive* h, int32_t* level, double* theta_main, double* theta_aux,
                        int64_t* snaps_main, int64_t* snaps_aux);
 
+/* ---- AERO binary stream files (streams.cpp:105-168, streams.hpp:45-47:
+ * load_stream / save_stream with StreamFormat::Aero): "AERO", version 0x01,
+ * u32 d, u64 n (0 = until EOF), n rows of d LE fp64. Read in chunks (the
+ * configs' inputs do not fit in memory); FormatError (AERO_FORMAT_ERROR) for
+ * bad magic / version, truncated header or row, zero dimension, non-finite
+ * value -- raised by the chunk that holds it. */
+typedef struct aero_file aero_file;
+int aero_file_open(const char* path, aero_file** out, int32_t* d, uint64_t* n_header);
+/* next rows (max_rows x d row-major) -> *got (0 at the end) */
+int aero_file_read(aero_file* h, double* rows, int64_t max_rows, int64_t* got);
+int aero_file_close(aero_file* h);
+int aero_file_write(const char* path, const double* rows, int64_t n, int32_t d);
+/* stream a file through a sketch: row q gets t0 + q; chunk k+1 is read into a
+ * pinned buffer by a reader thread while chunk k is absorbed (n sequential
+ * updates, like aero_update_block). log_out (nullable) holds log_cap events;
+ * *rows_out = rows absorbed. */
+int aero_update_from_file(aero_sketch* h, const char* path, int64_t t0, int64_t chunk_rows,
+                          aero_event* log_out, int64_t log_cap, int64_t* rows_out);
+
 /* ---- stream generators (BASELINE.json configs; DESIGN.md GENERATOR spec) */
 typedef struct aero_gen_params {
     int32_t d, k, k2, _pad;

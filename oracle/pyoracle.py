@@ -710,3 +710,39 @@ def gen_amm_rows(seed, dx, dy, latent, noise, r_max, t0, n):
     x, y = np.empty((n, dx)), np.empty((n, dy))
     _chk(lib().orc_gen_amm_rows(seed, dx, dy, latent, noise, r_max, t0, n, _dp(x), _dp(y)))
     return x, y
+
+
+# ------------------------------------------------------------------ AERO files
+def aero_bytes(rows):
+    """save_stream(..., StreamFormat::Aero) restated (reference streams.cpp:150-168):
+    'AERO', version 0x01, u32 d, u64 n, rows as little-endian fp64 row-major."""
+    rows = np.ascontiguousarray(rows, "<f8")
+    n, d = rows.shape
+    return b"AERO" + bytes([1]) + np.uint32(d).tobytes() + np.uint64(n).tobytes() + rows.tobytes()
+
+
+def load_aero_bytes(buf):
+    """load_aero restated (reference streams.cpp:107-137); raises FormatError."""
+    if len(buf) < 4 or buf[:4] != b"AERO":
+        raise FormatError("bad magic")
+    if len(buf) < 5 or buf[4] != 1:
+        raise FormatError("unsupported version")
+    if len(buf) < 17:
+        raise FormatError("truncated header")
+    d = int(np.frombuffer(buf[5:9], "<u4")[0])
+    n = int(np.frombuffer(buf[9:17], "<u8")[0])
+    if d == 0:
+        raise FormatError("zero dimension")
+    body = buf[17:]
+    rb = 8 * d
+    avail = len(body) // rb
+    if n == 0:
+        if len(body) % rb:
+            raise FormatError(f"truncated row {avail + 1}")
+        n = avail
+    elif avail < n:
+        raise FormatError(f"truncated row {avail + 1}")
+    rows = np.frombuffer(body[:n * rb], "<f8").reshape(n, d).copy()
+    if not np.all(np.isfinite(rows)):
+        raise FormatError("non-finite value")
+    return rows

@@ -5,4 +5,5 @@ this package is its host-side mirror of the reference C++ API.
 """
 from .capi import (AdaptiveState, AeroState, AttpState, CodState, Coordinator, CudaError, InvalidInput, MlState,  # noqa: F401
                    ProtocolError, dev_product, dist_theta_schedule, eigh, gen_rows_device, kernel_launches, lib,
-                   nccl_comm_init, nccl_unique_id, rng_gaussians, rng_gaussians_host)
+                   nccl_comm_init, nccl_unique_id, read_aero, rng_gaussians, rng_gaussians_host,
+                   write_aero, AeroFileReader)

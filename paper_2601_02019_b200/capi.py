@@ -110,6 +110,11 @@ SIGNATURES = [
     ("aero_set_theta", i32, [vp, f64]),
     ("aero_set_rng_fill", i32, [vp, vp, vp]),
     ("aero_update_block", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
+    ("aero_file_open", i32, [C.c_char_p, P(vp), P(i32), P(u64)]),
+    ("aero_file_read", i32, [vp, P(f64), i64, P(i64)]),
+    ("aero_file_close", i32, [vp]),
+    ("aero_file_write", i32, [C.c_char_p, P(f64), i64, i32]),
+    ("aero_update_from_file", i32, [vp, C.c_char_p, i64, i64, P(Event), i64, P(i64)]),
     ("aero_update_block_device", i32, [vp, vp, i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_update_block_amplified", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_query", i32, [vp, i64, i64, P(f64)]),
@@ -411,6 +416,24 @@ class AeroState:
         _chk(lib().aero_query(self._h, lb, ub, _dp(out)))
         return out
 
+    def update_from_file(self, path, t0=None, chunk_rows=16384, want_log=False):
+        """Stream an AERO file through the sketch (streams.cpp:105-137 format):
+        row q gets timestamp t0 + q (default: clock + 1); the next chunk is
+        read from disk while the current one is absorbed. Returns the events
+        (want_log) or the row count."""
+        t0 = self.clock + 1 if t0 is None else int(t0)
+        cap = 0
+        ev = None
+        if want_log:
+            with AeroFileReader(path) as f:
+                cap = f.n_header or sum(1 for _ in f.chunks(65536)) * 65536
+            ev = (Event * max(cap, 1))()
+        got = i64()
+        _chk(lib().aero_update_from_file(self._h, os.fsencode(path), t0, chunk_rows, ev, cap, C.byref(got)))
+        if want_log:
+            return np.frombuffer(ev, dtype=EVENT_DTYPE, count=got.value).copy()
+        return got.value
+
     def query_gram(self, lb, ub):
         out = np.empty((self.d, self.d))
         _chk(lib().aero_query_gram(self._h, lb, ub, _dp(out)))
@@ -466,6 +489,62 @@ class AeroState:
 
     def reset_profile(self):
         _chk(lib().aero_reset_profile(self._h))
+
+
+class AeroFileReader:
+    """Chunked reader of an AERO stream file (reference load_stream with
+    StreamFormat::Aero, streams.cpp:105-137): header validated on open,
+    FormatError for truncated or non-finite rows."""
+
+    def __init__(self, path):
+        h, d, n = vp(), i32(), u64()
+        _chk(lib().aero_file_open(os.fsencode(path), C.byref(h), C.byref(d), C.byref(n)))
+        self._h, self.d, self.n_header = h, d.value, n.value
+
+    def read(self, max_rows):
+        out = np.empty((max(max_rows, 0), self.d))
+        got = i64()
+        _chk(lib().aero_file_read(self._h, _dp(out), max_rows, C.byref(got)))
+        return out[:got.value]
+
+    def chunks(self, rows=65536):
+        while True:
+            blk = self.read(rows)
+            if blk.shape[0] == 0:
+                return
+            yield blk
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().aero_file_close(self._h)
+        self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def read_aero(path):
+    """All rows of an AERO file as an (n, d) array."""
+    with AeroFileReader(path) as f:
+        parts = list(f.chunks())
+        return np.concatenate(parts) if parts else np.empty((0, f.d))
+
+
+def write_aero(path, rows):
+    """save_stream(..., StreamFormat::Aero) (streams.cpp:150-168)."""
+    rows = _f64(rows)
+    if rows.ndim != 2 or rows.shape[0] == 0:
+        raise InvalidInput("save_stream: empty record set")
+    _chk(lib().aero_file_write(os.fsencode(path), _dp(rows), rows.shape[0], rows.shape[1]))
 
 
 class AttpState(AeroState):

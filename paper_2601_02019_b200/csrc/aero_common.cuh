@@ -15,6 +15,9 @@ namespace aero_b200 {
 struct InvalidInput : std::invalid_argument {
     explicit InvalidInput(const std::string& w) : std::invalid_argument(w) {}
 };
+struct FormatError : std::runtime_error {  // errors.hpp: malformed stream file
+    using std::runtime_error::runtime_error;
+};
 struct ProtocolError : std::runtime_error {
     explicit ProtocolError(const std::string& w) : std::runtime_error(w) {}
 };

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "aero_common.cuh"
+#include "aeroio.hpp"
 #include "engines.hpp"
 #include "sketch.hpp"
 #include "rng_panels.hpp"
@@ -33,6 +34,9 @@ int guard(F&& f) {
     } catch (const ProtocolError& e) {
         g_last_error = e.what();
         return AERO_PROTOCOL_ERROR;
+    } catch (const FormatError& e) {
+        g_last_error = e.what();
+        return AERO_FORMAT_ERROR;
     } catch (const CudaError& e) {
         g_last_error = e.what();
         return AERO_CUDA_ERROR;
@@ -593,6 +597,47 @@ int aero_adaptive_info(aero_adaptive* h, int32_t* level, double* theta_main, dou
     if (snaps_main) *snaps_main = h->e->main().snap_count();
     if (snaps_aux) *snaps_aux = h->e->aux().snap_count();
     return AERO_OK;
+}
+
+// ---- AERO files ------------------------------------------------------------------
+struct aero_file {
+    AeroFile* f;
+};
+int aero_file_open(const char* path, aero_file** out, int32_t* d, uint64_t* n_header) {
+    REQ(path);
+    REQ(out);
+    return guard([&] {
+        AeroFile* f = new AeroFile(path);
+        if (d) *d = (int32_t)f->d();
+        if (n_header) *n_header = f->n_header();
+        *out = new aero_file{f};
+    });
+}
+int aero_file_read(aero_file* h, double* rows, int64_t max_rows, int64_t* got) {
+    REQ(h);
+    REQ(got);
+    if (max_rows > 0) REQ(rows);
+    return guard([&] { *got = h->f->read(rows, max_rows); });
+}
+int aero_file_close(aero_file* h) {
+    if (!h) return AERO_OK;
+    delete h->f;
+    delete h;
+    return AERO_OK;
+}
+int aero_file_write(const char* path, const double* rows, int64_t n, int32_t d) {
+    REQ(path);
+    if (n > 0) REQ(rows);
+    return guard([&] { aero_file_write(std::string(path), rows, n, d); });
+}
+int aero_update_from_file(aero_sketch* h, const char* path, int64_t t0, int64_t chunk_rows,
+                          aero_event* log_out, int64_t log_cap, int64_t* rows_out) {
+    REQ(h);
+    REQ(path);
+    return guard([&] {
+        const int64_t n = aero_file_update(*h->s, path, t0, chunk_rows, log_out, log_cap);
+        if (rows_out) *rows_out = n;
+    });
 }
 
 // ---- generator -----------------------------------------------------------------

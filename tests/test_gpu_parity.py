@@ -879,3 +879,28 @@ def test_adaptive_state_matches_oracle(orc, dx, dy, eps, theta0, n, T, blk):
     a, bb = s.query()
     ar, br = ref.query()
     assert rel_fro(a @ bb.T, ar @ br.T) < 1e-7
+
+
+def test_update_from_aero_file_matches_update_block(orc, tmp_path):
+    """The streamed AERO file path (reader thread + pinned double buffer,
+    streams.cpp:105-137 format) absorbs exactly what update_block does on the
+    same rows: identical trace and sketch; a non-finite value in a later chunk
+    raises FormatError after the earlier chunks were absorbed."""
+    d, n = 24, 2500
+    rows = orc.gen_rows(d, 6, 0.9, 0.1, 64.0, 4, 0, 1, n)
+    p = tmp_path / "rows.aero"
+    prod.write_aero(p, rows)
+    a = prod.AttpState(d, 0.2, seed=4, stream=1000)
+    ev_a = a.update_from_file(p, chunk_rows=1000, want_log=True)
+    b = prod.AttpState(d, 0.2, seed=4, stream=1000)
+    ev_b = b.update_block(rows, np.arange(1, n + 1))
+    assert_trace_equal(ev_a, ev_b, rtol=0.0)
+    assert np.array_equal(a.query_gram(0, n), b.query_gram(0, n))
+    bad = rows.copy()
+    bad[2200, 3] = np.nan
+    q = tmp_path / "bad.aero"
+    q.write_bytes(orc.aero_bytes(np.nan_to_num(bad, nan=0.0))[:17] + bad.astype("<f8").tobytes())
+    c = prod.AttpState(d, 0.2, seed=4, stream=1000)
+    with pytest.raises(prod.capi.FormatError):
+        c.update_from_file(q, chunk_rows=1000)
+    assert c.clock == 2000
