@@ -558,13 +558,13 @@ size_t sytrd_cluster_smem(int n, int cs) {
 //      alpha = -tau/2 w.v, w += alpha v, and x_{j+1} = row j+1 - v w_{j+1} - w v_{j+1}
 // y and the next column are double-buffered by column parity: a CTA can only
 // overwrite a buffer after every CTA passed the barrier that follows its reads.
-constexpr int SR_NT = 512;  // threads per CTA
-constexpr int SR_M = 4;     // column indices per thread (n <= SR_NT * SR_M)
 constexpr int SR_R = 14;    // rows per CTA (smem: 14 x 2048 doubles)
-constexpr int SR_NW = SR_NT / 32;
-constexpr int kSytrdRowsMax = SR_NT * SR_M;
+constexpr int SR_NWMAX = 16;  // warps per CTA (<= 512 threads)
+constexpr int kSytrdRowsMax = 2048;
 
-size_t sytrd_rows_smem(int n, int R) { return sizeof(double) * ((size_t)R * n + SR_NW * 16 + 2 * SR_R + 8); }
+size_t sytrd_rows_smem(int n, int R) {
+    return sizeof(double) * ((size_t)R * n + SR_NWMAX * 16 + 2 * SR_NWMAX + 2 * SR_R + 8);
+}
 
 struct SrArgs {
     int n, lda, R;
@@ -572,6 +572,7 @@ struct SrArgs {
     double *V, *d, *e, *tau;
     double *ypub, *cpub;  // 2 x n each
     unsigned* bar;
+    unsigned long long* prof;  // optional (AERO_SYTRD_PROF): CTA 0 ns per segment
 };
 
 // sum of 16 per-thread values over a warp by recursive halving (16 shuffles
@@ -610,15 +611,33 @@ __device__ __forceinline__ int warp_sum16_index(int lane) {
     return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
 }
 
+// one-barrier block sum: the caller alternates buffers so that a buffer is
+// rewritten only after another __syncthreads (fixed order: deterministic)
+template <int NW>
+__device__ __forceinline__ double block_sum1(double v, double* buf) {
+    v = warp_sum_d(v);
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += buf[w];
+    return s;
+}
+
+template <int SR_NT>
 __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
+    constexpr int SR_M = kSytrdRowsMax / SR_NT;  // column indices per thread
+    constexpr int SR_NW = SR_NT / 32;
     extern __shared__ __align__(16) double sm[];
     const int n = a.n, G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int R = a.R;
     const int nr = (n - cta + G - 1) / G;  // own rows r_k = cta + G k, k < nr (<= R)
     double* As = sm;                        // nr x n, row k at As + k n
-    double* red = sm + (size_t)R * n;       // SR_NW x 16
-    double* rv = red + SR_NW * 16;          // v_{j-1}(r_k)
+    double* red = sm + (size_t)R * n;       // SR_NW x 16 (row sums)
+    double* rs2 = red + SR_NWMAX * 16;      // SR_NW: reflector norm partials
+    double* rdot = rs2 + SR_NWMAX;          // SR_NW: w.v partials
+    double* rv = rdot + SR_NWMAX;           // v_{j-1}(r_k)
     double* rw = rv + SR_R;                 // w_{j-1}(r_k)
     double* bc = rw + SR_R;                 // broadcast scalars
     for (int k = 0; k < nr; ++k) {
@@ -634,6 +653,16 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
         vr[m] = wr[m] = 0.0;
     }
     unsigned epoch = 0;
+    const bool pr = a.prof && cta == 0 && tid == 0;
+    unsigned long long tp = 0;
+    if (pr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp));
+#define SR_MARK(i)                                                   \
+    if (pr) {                                                        \
+        unsigned long long t_;                                       \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));       \
+        a.prof[i] += t_ - tp;                                        \
+        tp = t_;                                                     \
+    }
     for (int j = 0; j < n - 1; ++j) {
         // ---- 1. reflector (dlarfg) from x_j, rows j+1 ..
         double s2 = 0.0;
@@ -644,7 +673,7 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
             if (cc == j) bc[0] = xr[m];
             if (cc == j + 1) bc[1] = xr[m];
         }
-        s2 = block_sum_d(s2, red);  // syncs: bc visible
+        s2 = block_sum1<SR_NW>(s2, rs2);  // the sync also publishes bc
         const double dj = bc[0], alpha = bc[1];
         double tj = 0.0, beta = alpha, scal = 0.0;
         if (s2 > 0.0) {
@@ -665,27 +694,33 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
             a.e[j] = beta;
             a.tau[j] = tj;
         }
+        SR_MARK(0);
         // ---- 2. fused pass: pending update j-1, then y = A v_j (own rows >= j+1)
         const int k0 = (j + 1 <= cta) ? 0 : (j + 1 - cta + G - 1) / G;  // first own row >= j+1
         double acc[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        bool act[SR_M];
 #pragma unroll
-        for (int m = 0; m < SR_M; ++m) {
-            const int cc = tid + SR_NT * m;
-            if (cc >= j + 1 && cc < n) {
-                const double vo = vr[m], wo = wr[m], vj = vn[m];
+        for (int m = 0; m < SR_M; ++m) act[m] = (tid + SR_NT * m >= j + 1) && (tid + SR_NT * m < n);
 #pragma unroll
-                for (int k = 0; k < SR_R; ++k) {
-                    if (k >= k0 && k < nr) {
-                        double* p = As + (size_t)k * n + cc;
-                        const double x = fma(-rw[k], vo, fma(-rv[k], wo, *p));
+        for (int k = 0; k < SR_R; ++k) {
+            if (k >= k0 && k < nr) {
+                // row factors once per row (stores to As could alias them otherwise)
+                const double rvk = rv[k], rwk = rw[k];
+                double* rowp = As + (size_t)k * n + tid;
+#pragma unroll
+                for (int m = 0; m < SR_M; ++m) {
+                    if (act[m]) {
+                        double* p = rowp + SR_NT * m;
+                        const double x = fma(-rwk, vr[m], fma(-rvk, wr[m], *p));
                         *p = x;
-                        acc[k] = fma(x, vj, acc[k]);
+                        acc[k] = fma(x, vn[m], acc[k]);
                     }
                 }
             }
         }
+        SR_MARK(1);
         // row j+1 after updates <= j-1 is the next column (symmetry): publish it
         double* cpub = a.cpub + (size_t)(j & 1) * n;
         double* ypub = a.ypub + (size_t)(j & 1) * n;
@@ -701,7 +736,6 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
         {
             const double ws = warp_sum16(acc, lane);
             const int idx = warp_sum16_index(lane);
-            __syncthreads();  // red: the reflector's block sum is read by now
             if (!(lane & 1)) red[warp * 16 + idx] = ws;
             __syncthreads();
             if (tid < nr && tid >= k0) {
@@ -710,7 +744,9 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
                 __stcg(ypub + cta + G * tid, y);
             }
         }
+        SR_MARK(2);
         grid_sync(a.bar, epoch, G);
+        SR_MARK(3);
         // ---- 4. w = tau y; alpha = -tau/2 w.v; w += alpha v; next column
         double yv[SR_M], cv[SR_M];
 #pragma unroll
@@ -727,7 +763,7 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
             dot = fma(yv[m], vn[m], dot);
             if (tid + SR_NT * m == j + 1) bc[2] = yv[m];
         }
-        dot = block_sum_d(dot, red);
+        dot = block_sum1<SR_NW>(dot, rdot);
         const double al = -0.5 * tj * dot;
         const double vj1 = (tj != 0.0) ? 1.0 : 0.0;
         const double wj1 = bc[2] + al * vj1;
@@ -743,7 +779,9 @@ __global__ void __launch_bounds__(SR_NT, 1) k_sytrd_rows(SrArgs a) {
                 rw[cc / G] = wn;
             }
         }
+        SR_MARK(4);
     }
+#undef SR_MARK
     // x_{n-1}(n-1): the last diagonal element
 #pragma unroll
     for (int m = 0; m < SR_M; ++m)
@@ -1392,7 +1430,9 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sytrd_cluster_smem(kSytrdClusterMax, 16)));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_rows<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sytrd_rows_smem(kSytrdRowsMax, SR_R)));
+        AERO_CUDA(cudaFuncSetAttribute(k_sytrd_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sytrd_rows_smem(kSytrdRowsMax, SR_R)));
         AERO_CUDA(cudaFuncSetAttribute(k_sytrd_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * (kSytrdSmall * kSytrdSmall + 2 * kSytrdSmall + 64))));
@@ -1486,13 +1526,27 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
         // matrix resident in shared memory, one grid barrier per column
         const int Gr = wk.grid, R = (n + Gr - 1) / Gr;
         wk.pub.alloc((size_t)4 * n);
-        SrArgs sa{n, lda, R, A, wk.V.p, d, e, tau, wk.pub.p, wk.pub.p + 2 * (size_t)n, wk.bar};
+        SrArgs sa{n, lda, R, A, wk.V.p, d, e, tau, wk.pub.p, wk.pub.p + 2 * (size_t)n, wk.bar, prof};
         void* sargs[] = {&sa};
-        AERO_CUDA(cudaLaunchCooperativeKernel((void*)k_sytrd_rows, dim3(Gr), dim3(SR_NT), sargs,
-                                              sytrd_rows_smem(n, R), st));
+        static const int nt_env = getenv("AERO_SYTRD_NT") ? atoi(getenv("AERO_SYTRD_NT")) : 512;  // dev A/B
+        if (nt_env == 256)
+            AERO_CUDA(cudaLaunchCooperativeKernel((void*)k_sytrd_rows<256>, dim3(Gr), dim3(256), sargs,
+                                                  sytrd_rows_smem(n, R), st));
+        else
+            AERO_CUDA(cudaLaunchCooperativeKernel((void*)k_sytrd_rows<512>, dim3(Gr), dim3(512), sargs,
+                                                  sytrd_rows_smem(n, R), st));
     } else {
         AERO_CUDA(cudaLaunchCooperativeKernel(vec ? (void*)k_sytrd<true> : (void*)k_sytrd<false>, dim3(G),
                                               dim3(TRD_THREADS), args, smem, st));
+    }
+    if (prof && n <= kSytrdRowsMax && !no_rows) {
+        unsigned long long h[16];
+        AERO_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+        AERO_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "sytrd_rows n=%d us: reflector %.0f pass %.0f rowsum+publish %.0f barrier %.0f update+next %.0f\n",
+                n, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3);
+        cudaFree(prof);
+        prof = nullptr;
     }
     if (prof) {
         unsigned long long h[16];

@@ -357,6 +357,42 @@ def test_ml_bookkeeping_bit_exact(orc, n_win, scale_rows):
         assert sum(s.heavy_count(j) for j in range(s.levels)) > 0
 
 
+def test_c3_scaled_indexing_parity_fixture(orc):
+    """SURVEY.md 8(d)'s scaled C3 variant run to completion: MlState with the
+    C3 parameters (d=1024, eps=1/64, R=1024, 10 levels) but window N=4096 over
+    n=32768 rows (basis re-drawn every 2N), against the oracle's run
+    (tests/golden/c3_scaled.npz, tools/make_c3_fixture.py). Every 1024 rows:
+    every level's snapshot queue (s, t, xi) and heavy rows (s, t) bit-exact,
+    the query's level / fallback / xi_sum / heavy_used bit-exact, window
+    covariance error within 1e-6 of the oracle's (sliding_window.cpp:67-146)."""
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "c3_scaled.npz")
+    if not os.path.exists(p):
+        pytest.skip("tests/golden/c3_scaled.npz missing (tools/make_c3_fixture.py)")
+    fx = np.load(p)
+    D, N, NROWS, DRIFT, PROBE = (int(x) for x in fx["params"])
+    rows = orc.gen_rows(D, 64, 0.9, 0.1, 1024.0, 1, 0, 1, NROWS, drift=DRIFT)
+    ts = np.arange(1, NROWS + 1, dtype=np.int64)
+    s = prod.MlState(D, N, 1024.0, 1 / 64, seed=1, stream=1000)
+    meta = fx["meta"]
+    dev = torch.from_numpy(rows).cuda()
+    for p_i, b in enumerate(range(0, NROWS, PROBE)):
+        s.update_block(dev[b:b + PROBE], ts[b:b + PROBE])
+        mine = []
+        for j in range(s.levels):
+            mine += [(p_i, j, 0, x[1], x[2], x[0]) for x in s.level_state(j).snap_meta()]
+            mine += [(p_i, j, 1, h["s"], h["t"], 0) for h in s.heavy(j)]
+        theirs = [tuple(int(v) for v in r) for r in meta[meta[:, 0] == p_i]]
+        assert sorted(mine) == sorted(theirs), p_i
+        q = s.query()
+        assert (q["level"], int(q["fallback"]), q["xi_sum"], q["heavy_used"]) == tuple(int(v) for v in fx["query"][p_i])
+        lo = max(0, b + PROBE - N)
+        w = dev[lo:b + PROBE]
+        bt = torch.from_numpy(q["sketch"]).cuda()
+        err = float(torch.linalg.eigvalsh(w.T @ w - bt.T @ bt).abs().max()) / float((w * w).sum())
+        assert abs(err - fx["err"][p_i]) <= 1e-6, (p_i, err, fx["err"][p_i])
+
+
 # ---------------------------------------------------------------- eigensolver
 @pytest.mark.parametrize("n", [2, 7, 32, 64, 96, 97, 128, 256, 301, 512, 513, 777, 1024, 1536, 2048])
 def test_eigh_matches_oracle(orc, n):
