@@ -35,14 +35,14 @@ CONFIGS = {
                name="C2 tight-eps persistent stream n=1048576 d=4096 eps=1/512 "
                     "(k=256, sigma=0.99^j, noise 0.05, R=256)"),
     "c3": dict(kind="sw", d=1024, eps=1 / 64, k=64, rho=0.9, noise=0.1, r_max=1024.0, n=1048576,
-               window=65536, drift=131072, rows_per_step=4096, cpu_rows=600,
+               window=65536, drift=131072, rows_per_step=8192, cpu_rows=600, steady_rows=131072,
                name="C3 sliding window N=65536 n=1048576 d=1024 eps=1/64 R=1024 (k=64, drift 131072)"),
     "c4": dict(kind="dist", d=2048, eps=1 / 128, k=128, rho=0.97, noise=0.1, r_max=64.0, n=1048576,
                k2=16, rho2=0.9, scale2=0.5, rows_per_step=4096, cpu_rows=300, sites=8,
                name="C4 distributed, m=8 sites spread over the GPUs (one per GPU at 8), d=2048 eps=1/128 "
                     "(global k=128 + site k=16, noise 0.1, R=64)"),
     "c5": dict(kind="amm", dx=1024, dy=768, d=1024, eps=1 / 64, latent=48, noise=0.1, r_max=64.0,
-               n=1048576, window=65536, rows_per_step=512, cpu_rows=200,
+               n=1048576, window=65536, rows_per_step=4096, cpu_rows=200, steady_rows=65536,
                name="C5 sliding-window AMM dx=1024 dy=768 N=65536 eps=1/64 (latent 48, noise 0.1)"),
 }
 
@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-steady", action="store_true",
+                    help="C3/C5: skip the untimed steady-state prefix (2N / N rows)")
     ap.add_argument("--rng", default="device", choices=["device", "host"],
                     help="random projections drawn on the device, or on the host and uploaded "
                          "(AERO_FLAG_HOST_RNG: bit-identical to the reference's rng.hpp)")
@@ -352,7 +354,12 @@ def run_other(args, cfg, world, rank, local):
         dist.init_process_group("nccl", device_id=dev)
     S = args.rows_per_step or cfg["rows_per_step"]
     steps, warm = args.steps, args.warmup
-    nrows = S * (steps + warm)
+    # untimed prefix that brings the window configs to steady state before the
+    # W warm-up steps: C3 2N rows (window expiry, level caps, the first drift
+    # epoch at 131072), C5 N rows (expiry of snapshots)
+    pre = 0 if args.no_steady else cfg.get("steady_rows", 0)
+    pre = (pre + S - 1) // S  # in steps
+    nrows = S * (pre + steps + warm)
     kind = cfg["kind"]
     ts_all = np.arange(1, nrows + 1, dtype=np.int64)
     def barrier():
@@ -363,14 +370,14 @@ def run_other(args, cfg, world, rank, local):
     def timed(upd):
         """W warm-up steps, then K steps bracketed by barrier + CUDA events on the
         current stream (every update_block returns after its own streams finished)."""
-        for w in range(warm):
+        for w in range(pre + warm):
             upd(slice(w * S, (w + 1) * S))
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = prod.kernel_launches()
         with ClockSampler(local) as clk:
             e0.record()
-            for k in range(warm, warm + steps):
+            for k in range(pre + warm, pre + warm + steps):
                 upd(slice(k * S, (k + 1) * S))
             e1.record()
             e1.synchronize()
@@ -477,7 +484,7 @@ def run_other(args, cfg, world, rank, local):
             "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True,
             "scaling": "strong" if kind == "dist" else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg["name"], "rows_per_step": S, "timed_rows": f"{warm * S + 1}..{nrows}",
+            "config": {"workload": cfg["name"], "rows_per_step": S, "timed_rows": f"{(pre + warm) * S + 1}..{nrows}",
                        "parallelism": (f"sites={unit_rows} over {world} GPU(s) ({unit_rows // world} per GPU), "
                                        f"ncclReduce merge") if kind == "dist" else "single"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

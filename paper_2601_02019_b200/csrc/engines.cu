@@ -85,6 +85,14 @@ void MlEngine::pop_front(int j) {
     }
 }
 
+MlEngine::~MlEngine() {
+    cudaSetDevice(dev_);
+    for (auto& l : levels_) l->synchronize();
+    if (bad_d_) cudaFree(bad_d_);
+    for (int64_t* p : gidx_d_)
+        if (p) cudaFree(p);
+}
+
 // sliding_window.cpp:67-100. Level sketches ingest their (non-heavy) rows of
 // a block concurrently (one host thread + CUDA stream per level); the
 // combined-queue bookkeeping (expiry, heavy routing, cap) is then replayed
@@ -98,10 +106,15 @@ void MlEngine::update_block(const double* rows, bool device, int64_t n, int64_t 
     stage_.alloc((size_t)S * d_);
     nrm_.alloc(S);
     std::vector<double> nrm_h(S);
-    int* bad_d = nullptr;
-    AERO_CUDA(cudaMalloc(&bad_d, sizeof(int) * S));
+    if (!bad_d_) AERO_CUDA(cudaMalloc(&bad_d_, sizeof(int) * S));
+    int* bad_d = bad_d_;
     std::vector<int> bad_h(S);
     const int L = levels();
+    if ((int)gath_.size() < L) {
+        gath_.resize(L);
+        gidx_d_.resize(L, nullptr);
+        gidx_n_.resize(L, 0);
+    }
     for (int64_t off = 0; off < n; off += S) {
         const int64_t cnt = std::min(S, n - off);
         AERO_CUDA(cudaMemcpy2DAsync(stage_.p, sizeof(double) * d_, rows + off * ld,
@@ -127,7 +140,6 @@ void MlEngine::update_block(const double* rows, bool device, int64_t n, int64_t 
         // level sketches in parallel
         std::vector<std::exception_ptr> errs(L);
         std::vector<std::thread> th;
-        std::vector<DeviceBuf> gath(L);
         for (int lv = 0; lv < L; ++lv) {
             th.emplace_back([&, lv] {
                 try {
@@ -137,13 +149,18 @@ void MlEngine::update_block(const double* rows, bool device, int64_t n, int64_t 
                     std::vector<int64_t> ts(idx.size());
                     for (size_t q = 0; q < idx.size(); ++q) ts[q] = t[off + idx[q]];
                     const double* src = stage_.p;
-                    if ((int64_t)idx.size() != good) {  // gather the level's rows
-                        gath[lv].alloc(idx.size() * (size_t)d_);
-                        for (size_t q = 0; q < idx.size(); ++q)
-                            AERO_CUDA(cudaMemcpyAsync(gath[lv].p + q * d_, stage_.p + idx[q] * d_,
-                                                      sizeof(double) * d_, cudaMemcpyDeviceToDevice,
-                                                      levels_[lv]->stream()));
-                        src = gath[lv].p;
+                    if ((int64_t)idx.size() != good) {  // gather the level's rows (one kernel)
+                        gath_[lv].alloc(idx.size() * (size_t)d_);
+                        if (gidx_n_[lv] < idx.size()) {
+                            if (gidx_d_[lv]) cudaFree(gidx_d_[lv]);
+                            AERO_CUDA(cudaMalloc(&gidx_d_[lv], sizeof(int64_t) * S));
+                            gidx_n_[lv] = S;
+                        }
+                        cudaStream_t ls = levels_[lv]->stream();
+                        AERO_CUDA(cudaMemcpyAsync(gidx_d_[lv], idx.data(), sizeof(int64_t) * idx.size(),
+                                                  cudaMemcpyHostToDevice, ls));
+                        gather_rows(ls, stage_.p, d_, gidx_d_[lv], (int64_t)idx.size(), d_, gath_[lv].p);
+                        src = gath_[lv].p;
                     }
                     levels_[lv]->update_block(src, true, (int64_t)idx.size(), d_, ts.data(), nullptr,
                                               nullptr, amplified_);
@@ -190,12 +207,8 @@ void MlEngine::update_block(const double* rows, bool device, int64_t n, int64_t 
             rowbuf.clear();
             clock_ = i;
         }
-        if (good < cnt) {
-            cudaFree(bad_d);
-            throw InvalidInput(err);
-        }
+        if (good < cnt) throw InvalidInput(err);
     }
-    cudaFree(bad_d);
 }
 
 // sliding_window.cpp:102-146

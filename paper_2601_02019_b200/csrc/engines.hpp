@@ -21,6 +21,9 @@ class MlEngine {
   public:
     MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, uint64_t stream, int device,
              double delta = 0.0);
+    ~MlEngine();
+    MlEngine(const MlEngine&) = delete;
+    MlEngine& operator=(const MlEngine&) = delete;
     void update_block(const double* rows, bool device, int64_t n, int64_t ld, const int64_t* t);
     void query(double* out_host, aero_ml_query_result* res);
     void info(aero_ml_info* out) const;
@@ -47,6 +50,10 @@ class MlEngine {
     std::vector<LevelQueue> lq_;
     std::deque<double> ring_;
     DeviceBuf stage_, gather_, nrm_, out_, qa_, qb_;
+    int* bad_d_ = nullptr;                     // K1 finiteness flags (stage rows)
+    std::vector<DeviceBuf> gath_;              // per-level gathered rows
+    std::vector<int64_t*> gidx_d_;             // per-level gather indices (device)
+    std::vector<size_t> gidx_n_;
     cudaStream_t st_ = nullptr;
 };
 

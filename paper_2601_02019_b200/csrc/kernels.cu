@@ -210,6 +210,22 @@ void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int
     AERO_LAUNCHED();
 }
 
+// dst[q] = src[idx[q]] for n rows of d doubles (row-major, ld)
+__global__ void k_gather_rows(const double* __restrict__ src, int64_t lds, const int64_t* __restrict__ idx,
+                              int64_t n, int d, double* __restrict__ dst) {
+    const int64_t q = blockIdx.x;
+    if (q >= n) return;
+    const double* s = src + idx[q] * lds;
+    double* o = dst + q * (int64_t)d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) o[j] = s[j];
+}
+void gather_rows(cudaStream_t st, const double* src, int64_t lds, const int64_t* idx_d, int64_t n, int d,
+                 double* dst) {
+    if (n <= 0) return;
+    k_gather_rows<<<(unsigned)n, 256, 0, st>>>(src, lds, idx_d, n, d, dst);
+    AERO_LAUNCHED();
+}
+
 // ============================================================================
 // CTA-wide cyclic Jacobi for small symmetric matrices in shared memory
 // (round-robin parallel ordering; A, V column-major n x n, ld = n).
@@ -634,10 +650,21 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 e = (xm > 0.0) ? ilogb(xm) + 1 : 0;
                 if (tid == 0) xs.fe[jb.col] = e;
             }
-            for (int i = tid; i < r; i += nt) {
-                const double v = y[i] / nrm;
-                x[i] = v;
-                if (xs.b) ozaki_store_value<kOzSlices, kOzBN>(xs.b, xs.Kp, jb.col, i, v, e);
+            for (int i = tid; i < r; i += nt) x[i] = y[i] / nrm;
+            if (xs.b) {  // 8 consecutive entries per thread: one 8-byte store per slice
+                const int nkb = xs.Kp / kOzBK, tt = jb.col / kOzBN, rr = jb.col % kOzBN;
+                for (int k0 = 8 * tid; k0 < r; k0 += 8 * nt) {
+                    double xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xv[u] = (k0 + u < r) ? y[k0 + u] / nrm : 0.0;
+                    uint64_t pk[kOzSlices];
+                    ozaki_slice8_pow2<kOzSlices>(xv, e, pk);
+                    int8_t* blk = xs.b + ((int64_t)tt * nkb + k0 / kOzBK) * kOzSlices * kOzBN * kOzBK + rr * kOzBK +
+                                  ((((k0 % kOzBK) >> 4) ^ ((rr >> 1) & 3)) << 4) + (k0 & 15);
+#pragma unroll
+                    for (int q = 0; q < kOzSlices; ++q)
+                        *reinterpret_cast<uint64_t*>(blk + q * kOzBN * kOzBK) = pk[q];
+                }
             }
         } else {
             double s = 0.0;  // sigma1^2 = ||A x||^2 = x^T G x (linalg.cpp:119)
@@ -727,17 +754,41 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 if ((tid & 31) == 0) red[64 + b * 32 + (tid >> 5)] = mxb[b];
             }
             __syncthreads();
+            // stage the new iterate in shared memory (ysh is free: every thread
+            // is past the update loop), then slice 8 consecutive entries per
+            // thread into one 8-byte store per slice (was one byte store per
+            // slice and entry)
+            int eb[KM];
 #pragma unroll
             for (int b = 0; b < KM; ++b) {
                 if (b >= k) break;
                 double m = 0.0;
                 for (int w = 0; w < (nt + 31) / 32; ++w) m = fmax(m, red[64 + b * 32 + w]);
-                const int e = (m > 0.0) ? ilogb(m) + 1 : 0;
-                if (tid == 0) xs.fe[jb.col + b] = e;
+                eb[b] = (m > 0.0) ? ilogb(m) + 1 : 0;
+                if (tid == 0) xs.fe[jb.col + b] = eb[b];
 #pragma unroll
                 for (int u = 0; u < RU; ++u) {
                     const int i = tid + u * nt;
-                    if (i < r) ozaki_store_value<kOzSlices, kOzBN>(xs.b, xs.Kp, jb.col + b, i, hv[u][b], e);
+                    if (i < r) ysh[i + b * r] = hv[u][b];
+                }
+            }
+            __syncthreads();
+            const int nkb = xs.Kp / kOzBK;
+#pragma unroll
+            for (int b = 0; b < KM; ++b) {
+                if (b >= k) break;
+                const int cidx = jb.col + b, tt = cidx / kOzBN, rr = cidx % kOzBN;
+                for (int k0 = 8 * tid; k0 < r; k0 += 8 * nt) {
+                    double xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) xv[u] = (k0 + u < r) ? ysh[k0 + u + b * r] : 0.0;
+                    uint64_t pk[kOzSlices];
+                    ozaki_slice8_pow2<kOzSlices>(xv, eb[b], pk);
+                    int8_t* blk = xs.b + ((int64_t)tt * nkb + k0 / kOzBK) * kOzSlices * kOzBN * kOzBK + rr * kOzBK +
+                                  ((((k0 % kOzBK) >> 4) ^ ((rr >> 1) & 3)) << 4) + (k0 & 15);
+#pragma unroll
+                    for (int q = 0; q < kOzSlices; ++q)
+                        *reinterpret_cast<uint64_t*>(blk + q * kOzBN * kOzBK) = pk[q];
                 }
             }
         } else if (xs.b && !last) {

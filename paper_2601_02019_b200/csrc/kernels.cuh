@@ -57,6 +57,9 @@ struct OzakiGram {
 };
 int ozaki_slices();
 
+// dst[q] = src[idx_d[q]] (rows of d doubles, src row stride lds, dst contiguous)
+void gather_rows(cudaStream_t st, const double* src, int64_t lds, const int64_t* idx_d, int64_t n, int d,
+                 double* dst);
 // per-row squared norm and finiteness of n rows (row-major, ld) -> nrm2[n], bad[n]
 void ingest_rows(cudaStream_t st, const double* rows, int64_t n, int64_t ld, int d, double* nrm2,
                  int* bad);

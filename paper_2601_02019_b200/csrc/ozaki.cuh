@@ -31,6 +31,26 @@ __device__ __forceinline__ void ozaki_slice8(const double (&x)[8], int e, uint64
     }
 }
 
+// same bytes as ozaki_slice8, with the exact power-of-two scaling by one
+// multiply (|x| < 2^e, e far from the exponent limits) instead of scalbn
+template <int S>
+__device__ __forceinline__ void ozaki_slice8_pow2(const double (&x)[8], int e, uint64_t (&pk)[S]) {
+    const bool fast = e > -900 && e < 900;
+    const double sc = fast ? __longlong_as_double((long long)(1023 + 7 - e) << 52) : 0.0;
+#pragma unroll
+    for (int p = 0; p < S; ++p) pk[p] = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        double y = fast ? x[u] * sc : scalbn(x[u], 7 - e);  // |y| < 128
+#pragma unroll
+        for (int p = 0; p < S; ++p) {
+            const double sv = trunc(y);
+            y = (y - sv) * 128.0;
+            pk[p] |= (uint64_t)(uint8_t)(int8_t)(int)sv << (8 * u);
+        }
+    }
+}
+
 template <int S, int TR, int NV>
 __device__ inline void ozaki_slice_vectors(const double* __restrict__ v0, int ldv, int lim, int Kp, int i0,
                                            int8_t* __restrict__ out, int* __restrict__ ex, double* red) {
