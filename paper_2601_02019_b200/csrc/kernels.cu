@@ -675,6 +675,86 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
         return;
     }
     // simul: S = X^T Y (Gram of g = C'^T X), T = S^{-1/2}
+    double tq[KM * KM];  // T (scaled), in registers for the update below
+    bool fast = false;
+    if constexpr (KM == 2) fast = !last;
+    if (fast) {
+        // k <= 2, not the last phase: the 2x2 Gram reduced once, then every
+        // thread evaluates the closed-form eig and the clamp redundantly
+        // (the same operations thread 0 runs on the general path: same bits),
+        // no serial section and one barrier instead of five
+        double part[4] = {0.0, 0.0, 0.0, 0.0};
+        constexpr int RUG = 8;
+        for (int i0 = tid; i0 < r; i0 += RUG * nt) {
+            double p[RUG][2], q[RUG][2];
+#pragma unroll
+            for (int u = 0; u < RUG; ++u) {
+                const int i = i0 + u * nt;
+#pragma unroll
+                for (int a2 = 0; a2 < 2; ++a2) {
+                    p[u][a2] = (i < r && a2 < k) ? x[i + (int64_t)a2 * ldx] : 0.0;
+                    q[u][a2] = (i < r && a2 < k) ? y[i + (int64_t)a2 * ldy] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RUG; ++u)
+#pragma unroll
+                for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+                    for (int b2 = 0; b2 < 2; ++b2) part[a2 + b2 * 2] = fma(p[u][a2], q[u][b2], part[a2 + b2 * 2]);
+        }
+        const int lane = tid & 31, wid = tid >> 5, nw = (nt + 31) >> 5;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double v = warp_sum(part[e]);
+            if (lane == 0) red[wid * 16 + e] = v;
+        }
+        __syncthreads();
+        double s[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += red[w * 16 + e];
+            s[e] = t;
+        }
+        NJ_MARK(1);
+        double w0, w3, t00, t10, t01, t11;
+        if (k == 1) {
+            w0 = s[0];
+            w3 = 0.0;
+            t00 = 1.0;
+            t10 = t01 = t11 = 0.0;
+        } else {  // small_eig's closed-form 2x2 Jacobi rotation on W = sym(S)
+            const double a = 0.5 * (s[0] + s[0]), b = 0.5 * (s[2] + s[1]), cc = 0.5 * (s[3] + s[3]);
+            double cn = 1.0, sn = 0.0, t = 0.0;
+            if (fabs(b) > 1e-300) {
+                const double tau = (cc - a) / (2.0 * b);
+                t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                cn = 1.0 / sqrt(1.0 + t * t);
+                sn = t * cn;
+            }
+            w0 = a - t * b;
+            w3 = cc + t * b;
+            t00 = cn;
+            t10 = -sn;
+            t01 = sn;
+            t11 = cn;
+        }
+        const double lmax = (k == 1) ? fmax(0.0, w0) : fmax(fmax(0.0, w0), w3);
+        const bool ok0 = w0 > 0.0 && w0 > 1e-14 * lmax;
+        const double l0 = ok0 ? 1.0 / sqrt(w0) : 0.0;
+        double l1 = 0.0;
+        if (k == 2) {
+            const bool ok1 = w3 > 0.0 && w3 > 1e-14 * lmax;
+            l1 = ok1 ? 1.0 / sqrt(w3) : 0.0;
+        }
+        // T[e] *= lam[e / k]: column b scaled by lam_b
+        tq[0] = t00 * l0;
+        tq[1] = t10 * l0;
+        tq[2] = t01 * l1;
+        tq[3] = t11 * l1;
+        NJ_MARK(2);
+    } else {
     cta_gram<KM>(x, ldx, y, ldy, r, k, S, red);
     NJ_MARK(1);
     for (int e = tid; e < k * k; e += nt) {
@@ -699,7 +779,10 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     __syncthreads();
     for (int e = tid; e < k * k; e += nt) T[e] *= lam[e / k];
     __syncthreads();
+#pragma unroll
+    for (int e = 0; e < KM * KM; ++e) tq[e] = (e < k * k) ? T[e] : 0.0;
     NJ_MARK(2);
+    }
     // rows independent: [last: H = X T], X <- Y T; RU rows per thread per
     // round with all their loads issued first (one L2 round trip per round).
     // With xs (not last): the new columns are also sliced for the next product
@@ -734,8 +817,8 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
 #pragma unroll
                     for (int a = 0; a < KM; ++a) {
                         if (a < k) {
-                            hx = fma(xr[u][a], T[a + b * k], hx);
-                            hy = fma(yr[u][a], T[a + b * k], hy);
+                            hx = fma(xr[u][a], tq[a + b * k], hx);
+                            hy = fma(yr[u][a], tq[a + b * k], hy);
                         }
                     }
                     if (last) H[i + (int64_t)(jb.col + b) * ldx] = hx;

@@ -98,6 +98,7 @@ Sketch::Sketch(const aero_cfg& cfg) {
     kp_ = power_iter_count(d_);
     q_ = simul_q(d_, eps_si_);
     max_batch_ = cfg.max_batch > 0 ? cfg.max_batch : 192;
+    cfg_max_batch_ = cfg.max_batch;
     cur_batch_ = std::min(64, max_batch_);
     AERO_CUDA(cudaSetDevice(dev_));
     AERO_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
@@ -866,7 +867,15 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
         // is cheapest per row near B* = sqrt(2 alpha / (beta p))
         const double p = std::max(end_rate_, 1e-4);
         static const double two_alpha = getenv("AERO_BATCH_2ALPHA") ? atof(getenv("AERO_BATCH_2ALPHA")) : 52.0;
-        cur_batch_ = (int)std::clamp(std::sqrt(two_alpha / p), 16.0, (double)max_batch_);
+        // int8 iterate (r >= i8_min_rows_): cap a batch at one column per
+        // job slot of a 64-wide MMA tile row -- 3 x 64 columns (FIRE1: 3 per
+        // row) or 192 (NOFIRE) -- which also keeps the jobs <= the 148 CTAs, so
+        // no CTA normalizes two jobs in a phase (C2 sweep: 64 rows 1858 ms vs
+        // 192 rows 1938 ms per 40960 rows; 48: 2120, 96: 1909)
+        int cap = max_batch_;
+        if (i8_ && r_ + 1 >= i8_min_rows_ && persistent_ && cfg_max_batch_ == 0)
+            cap = std::min(cap, (!amp_ && fire_ema_ >= 0.5) ? 64 : 192);
+        cur_batch_ = (int)std::clamp(std::sqrt(two_alpha / p), 16.0, (double)cap);
         const int64_t B = std::min<int64_t>({(int64_t)cur_batch_, n - pos, room});
         const int64_t mp0 = mispredicts;
         const auto b0 = std::chrono::steady_clock::now();

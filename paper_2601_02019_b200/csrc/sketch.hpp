@@ -135,6 +135,7 @@ class Sketch {
     double theta_, fro_mass_ = 0.0;
     bool host_prof_ = getenv("AERO_HOST_PROF") != nullptr;  // dev instrumentation
     double prof_append_ms_ = 0.0, prof_iter_ms_ = 0.0;
+    int cfg_max_batch_ = 0;  // caller-set batch cap (0 = engine default)
     int64_t clock_ = 0, last_dump_t_ = 0;
     uint64_t forks_ = 0;
     int r_ = 0;

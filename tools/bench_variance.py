@@ -20,7 +20,8 @@ rows = torch.empty((n, cfg["d"]), dtype=torch.float64, device="cuda")
 prod.gen_rows_device(rows, 1, cfg["d"], cfg["k"], cfg["rho"], cfg["noise"], cfg["r_max"], seed=1)
 ts = np.arange(1, n + 1, dtype=np.int64)
 for rep in range(R):
-    sk = prod.AttpState(cfg["d"], cfg["eps"], seed=1, stream=1000)
+    sk = prod.AttpState(cfg["d"], cfg["eps"], seed=1, stream=1000,
+                        max_batch=int(__import__("os").environ.get("MAXB", "0")))
     for w in range(W):
         sk.update_block(rows[w * S:(w + 1) * S], ts[w * S:(w + 1) * S])
     sk.synchronize()
