@@ -13,6 +13,8 @@
 // final Rayleigh-Ritz uses the GA/GB-orthonormal basis (same subspace, same
 // Ritz values as the reference's Householder iteration up to rounding).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <deque>
@@ -347,10 +349,22 @@ __global__ void k_cod_mirror(int c0, int nb, double* G, int ld) {
 
 constexpr int COD_MAX_BATCH = 128;  // speculative gate jobs per launch
 
+// Snapshot storage: columns of consecutive snapshots packed into chunks of
+// kCodChunkCols columns (z, h, zm^T, mh arrays per chunk). Snapshots are born
+// and expire in time order, so chunks fill at the back and empty at the front;
+// an emptied chunk is kept for reuse (a cudaFree would synchronize the device
+// on every expiry -- the first version did 4 cudaMalloc + 4 cudaFree per
+// snapshot, and C5 dumps on most rows). Reuse is ordered by the engine stream.
+constexpr int kCodChunkCols = 1024;
+struct CodChunk {
+    double *z = nullptr, *h = nullptr, *zm_t = nullptr, *mh = nullptr;
+    int used = 0, live = 0;
+};
 struct CodSnap {
     int xi;
     int64_t s, t;
     double *z, *h, *zm_t, *mh;  // device: z dx x xi, h dy x xi, zm^T dy x xi, mh dx x xi
+    CodChunk* chunk;
 };
 
 struct CodEngine::Impl {
@@ -359,13 +373,70 @@ struct CodEngine::Impl {
     int64_t n, clock = 0, last_dump = 0;
     uint64_t seed, stream, forks = 0;
     int c = 0;
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr, st2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DeviceBuf A, B, GA, GB, A2, B2, sig, hv, work, ws, q1, q2, q3, pib, xs_d, ys_d, gws;
     int batch = 32;         // adaptive speculative batch (rows)
     double fire_ema = 0.0;  // moving average of gate fires (batch pattern prediction)
     CodJob* jobs_d = nullptr;
     int* status_d = nullptr;
     std::deque<CodSnap> snaps;
+    // dev instrumentation (AERO_HOST_PROF): wall ms in run() / dumps / reduces
+    bool hprof = getenv("AERO_HOST_PROF") != nullptr;
+    double t_run = 0, t_dump = 0, t_reduce = 0, t_total = 0, t_eiga = 0, t_eigb = 0, t_eigk = 0;
+    int64_t n_run = 0, n_dump = 0, n_reduce = 0, n_rows = 0;
+    std::deque<CodChunk*> chunks;  // live chunks, oldest first
+    std::vector<CodChunk*> spare;  // emptied chunks kept for reuse
+    CodSnap snap_alloc(int xi) {
+        if (chunks.empty() || chunks.back()->used + xi > kCodChunkCols) {
+            CodChunk* ch;
+            if (!spare.empty()) {
+                ch = spare.back();
+                spare.pop_back();
+            } else {
+                ch = new CodChunk;
+                const size_t nc = kCodChunkCols;
+                AERO_CUDA(cudaMalloc(&ch->z, sizeof(double) * dx * nc));
+                AERO_CUDA(cudaMalloc(&ch->h, sizeof(double) * dy * nc));
+                AERO_CUDA(cudaMalloc(&ch->zm_t, sizeof(double) * dy * nc));
+                AERO_CUDA(cudaMalloc(&ch->mh, sizeof(double) * dx * nc));
+            }
+            ch->used = ch->live = 0;
+            chunks.push_back(ch);
+        }
+        CodChunk* ch = chunks.back();
+        const size_t col = (size_t)ch->used;
+        ch->used += xi;
+        ch->live += xi;
+        CodSnap sn{};
+        sn.xi = xi;
+        sn.chunk = ch;
+        sn.z = ch->z + col * dx;
+        sn.h = ch->h + col * dy;
+        sn.zm_t = ch->zm_t + col * dy;
+        sn.mh = ch->mh + col * dx;
+        return sn;
+    }
+    void snap_release(const CodSnap& sn) {
+        sn.chunk->live -= sn.xi;
+        while (!chunks.empty() && chunks.front()->live == 0 && chunks.front() != chunks.back()) {
+            spare.push_back(chunks.front());
+            chunks.pop_front();
+        }
+    }
+    void free_chunks() {
+        std::vector<CodChunk*> all(chunks.begin(), chunks.end());
+        all.insert(all.end(), spare.begin(), spare.end());
+        for (CodChunk* ch : all) {
+            cudaFree(ch->z);
+            cudaFree(ch->h);
+            cudaFree(ch->zm_t);
+            cudaFree(ch->mh);
+            delete ch;
+        }
+        chunks.clear();
+        spare.clear();
+    }
     aero_event ev{};
 
     uint64_t fork_state(uint64_t f) const { return rng_state0(seed, fork_stream(stream, f)); }
@@ -395,6 +466,17 @@ struct CodEngine::Impl {
 
     // run jobs (<= 3) -> sig (host), status (host)
     void run(const CodJob* hj, int nj, double* sig_h, int* status_h) {
+        const auto t0 = std::chrono::steady_clock::now();
+        struct Acc {
+            Impl& s;
+            std::chrono::steady_clock::time_point t0;
+            ~Acc() {
+                if (s.hprof) {
+                    s.t_run += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                    s.n_run++;
+                }
+            }
+        } acc{*this, t0};
         AERO_CUDA(cudaMemcpyAsync(jobs_d, hj, sizeof(CodJob) * nj, cudaMemcpyHostToDevice, st));
         const size_t smem = sizeof(double) * (32 + 2 * (size_t)c * COD_KMAX + 3 * COD_KMAX * COD_KMAX +
                                               COD_KMAX + 64 +
@@ -421,6 +503,18 @@ struct CodEngine::Impl {
     // The core Ra Rb^T = La^{1/2} (Wa^T Wb) Lb^{1/2} (ra x rb); its SVD u s v^T
     // gives a' = Qa u w, b' = Qb v w with w = sqrt(max(s - s_ell, 0)) (fd.cpp:77-84).
     void cod_reduce() {
+        const auto t0 = std::chrono::steady_clock::now();
+        struct Acc {
+            Impl& s;
+            std::chrono::steady_clock::time_point t0;
+            ~Acc() {
+                if (s.hprof) {
+                    cudaStreamSynchronize(s.st);  // destructor: no throw
+                    s.t_reduce += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                    s.n_reduce++;
+                }
+            }
+        } acc{*this, t0};
         const int m = c;  // == 2 ell
         q1.alloc((size_t)m * m * 6 + 4 * (size_t)m);
         double* Wa = q1.p;
@@ -434,8 +528,30 @@ struct CodEngine::Impl {
         double* ls = lb + m;
         copy_matrix(st, m, m, GA.p, cap, Wa, m);
         copy_matrix(st, m, m, GB.p, cap, Wb, m);
+        auto lap = [&](double& acc) {
+            if (!hprof) return;
+            AERO_CUDA(cudaStreamSynchronize(st));
+            static thread_local std::chrono::steady_clock::time_point last;
+            const auto now = std::chrono::steady_clock::now();
+            acc += std::chrono::duration<double, std::milli>(now - last).count();
+            last = now;
+        };
+        double dummy = 0;
+        lap(dummy);
+        // the two Gram eigendecompositions are independent: GB's on a second
+        // stream, concurrently (each is a latency-bound chain of small launches)
+        if (!st2) {
+            AERO_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+            AERO_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            AERO_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        AERO_CUDA(cudaEventRecord(ev_fork, st));
+        AERO_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
         eigh(st, m, Wa, m, la);
-        eigh(st, m, Wb, m, lb);
+        eigh(st2, m, Wb, m, lb);
+        AERO_CUDA(cudaEventRecord(ev_join, st2));
+        AERO_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+        lap(t_eiga);
         std::vector<double> ha(m), hb(m);
         AERO_CUDA(cudaMemcpyAsync(ha.data(), la, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
         AERO_CUDA(cudaMemcpyAsync(hb.data(), lb, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
@@ -467,7 +583,9 @@ struct CodEngine::Impl {
         scale_columns(st, ra, rb, K, ra, q2.p + m);
         // SVD of K via eig(K K^T): u (ra x ra, descending), s^2
         dgemm(st, false, true, ra, ra, rb, 1.0, K, ra, K, ra, 0.0, T, ra);
+        lap(dummy);
         eigh(st, ra, T, ra, ls, 1, 0, std::min(ra, keep + 1));  // the kept directions (and the cut)
+        lap(t_eigk);
         std::vector<double> hl(ra);
         AERO_CUDA(cudaMemcpyAsync(hl.data(), ls, sizeof(double) * ra, cudaMemcpyDeviceToHost, st));
         AERO_CUDA(cudaStreamSynchronize(st));
@@ -569,17 +687,24 @@ CodEngine::~CodEngine() {
     if (!im_) return;
     cudaSetDevice(im_->dev);
     if (im_->st) cudaStreamSynchronize(im_->st);
-    for (auto& s : im_->snaps) {
-        cudaFree(s.z);
-        cudaFree(s.h);
-        cudaFree(s.zm_t);
-        cudaFree(s.mh);
-    }
+    if (im_->hprof && im_->n_rows > 0)
+        fprintf(stderr, "cod host: %lld rows %.1f ms total | run %.1f ms (%lld calls) | dumps %.1f ms (%lld) | reduces %.1f ms (%lld): eig GA %.1f GB %.1f core %.1f\n",
+                (long long)im_->n_rows, im_->t_total, im_->t_run, (long long)im_->n_run, im_->t_dump,
+                (long long)im_->n_dump, im_->t_reduce, (long long)im_->n_reduce, im_->t_eiga, im_->t_eigb,
+                im_->t_eigk);
+    im_->free_chunks();
     cudaFree(im_->jobs_d);
     cudaFree(im_->status_d);
     if (im_->st) {
         eigh_forget(im_->st);
         cudaStreamDestroy(im_->st);
+    }
+    if (im_->st2) {
+        cudaStreamSynchronize(im_->st2);
+        eigh_forget(im_->st2);
+        cudaStreamDestroy(im_->st2);
+        cudaEventDestroy(im_->ev_fork);
+        cudaEventDestroy(im_->ev_join);
     }
     delete im_;
 }
@@ -596,6 +721,18 @@ void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, 
     Impl& s = *im_;
     AERO_CUDA(cudaSetDevice(s.dev));
     if (nrows <= 0) return;
+    const auto tu0 = std::chrono::steady_clock::now();
+    struct AccU {
+        Impl& s;
+        std::chrono::steady_clock::time_point t0;
+        int64_t n;
+        ~AccU() {
+            if (s.hprof) {
+                s.t_total += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                s.n_rows += n;
+            }
+        }
+    } accu{s, tu0, nrows};
     int64_t good = nrows;
     std::string err;
     int64_t prev = s.clock;
@@ -620,12 +757,7 @@ void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, 
 
     auto expire = [&](int64_t i) {  // amm.cpp:48
         while (!s.snaps.empty() && s.snaps.front().t + s.n <= i) {
-            AERO_CUDA(cudaStreamSynchronize(s.st));
-            auto& f = s.snaps.front();
-            cudaFree(f.z);
-            cudaFree(f.h);
-            cudaFree(f.zm_t);
-            cudaFree(f.mh);
+            s.snap_release(s.snaps.front());
             s.snaps.pop_front();
         }
     };
@@ -674,12 +806,8 @@ void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, 
                 }
                 ev.xi = xi;
                 if (xi >= 1) {
-                    CodSnap sn{};
-                    sn.xi = xi;
-                    AERO_CUDA(cudaMalloc(&sn.z, sizeof(double) * s.dx * xi));
-                    AERO_CUDA(cudaMalloc(&sn.h, sizeof(double) * s.dy * xi));
-                    AERO_CUDA(cudaMalloc(&sn.zm_t, sizeof(double) * s.dy * xi));
-                    AERO_CUDA(cudaMalloc(&sn.mh, sizeof(double) * s.dx * xi));
+                    const auto td0 = std::chrono::steady_clock::now();
+                    CodSnap sn = s.snap_alloc(xi);
                     if (stz == JOB_ZERO) {
                         std::vector<double> I((size_t)s.dx * xi, 0.0), J((size_t)s.dy * xi, 0.0);
                         for (int j = 0; j < xi; ++j) {
@@ -713,6 +841,11 @@ void CodEngine::update_block(const double* xs, const double* ys, int64_t nrows, 
                     s.last_dump = i;
                     s.snaps.push_back(sn);
                     ev.dumped = 1;
+                    if (s.hprof) {
+                        AERO_CUDA(cudaStreamSynchronize(s.st));
+                        s.t_dump += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
+                        s.n_dump++;
+                    }
                 }
                 break;
             }

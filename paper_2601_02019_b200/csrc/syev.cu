@@ -1249,6 +1249,102 @@ __global__ void k_twisted(int n, int nvec, const double* __restrict__ d, const d
 // Vectors of different unreduced blocks have disjoint support (exactly
 // orthogonal); inside a block the eigenvalues are distinct.
 constexpr int kMaxCluster = 128;
+// Long runs (the noise floor of the AMM cod_reduce Grams: ~200 linked
+// eigenvalues at n = 256 cost 7 ms vector by vector from L2) are
+// re-orthonormalized by block classical Gram-Schmidt applied twice (BCGS2):
+// panels of PB vectors staged in shared memory, projected against all earlier
+// run members with two passes over them (W = Q^T P, P -= Q W), then
+// CGS2-orthonormalized inside the panel. Same span, orthonormal to working
+// precision; ~20x fewer dependent steps.
+constexpr int kPanelMin = 32, kPanelMaxN = 512, kPanelMaxRun = 512;
+__host__ __device__ constexpr int cluster_panel_width(int n) { return n <= 256 ? 32 : 16; }
+size_t cluster_orth_smem(int n) {
+    const int pb = cluster_panel_width(n);
+    // panel (n x PB) + W (run x PB, run <= nvec <= n): 128 KiB at n = 256 or 512
+    return sizeof(double) * (n <= kPanelMaxN ? std::max<size_t>((size_t)n, (size_t)2 * n * pb) : n);
+}
+__device__ void cluster_orth_panels(int n, int nvec, int q, int end, double* __restrict__ Z, double* sm,
+                                    double* red) {
+    const int PB = cluster_panel_width(n);
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    double* P = sm;           // n x PB, row t at P + t * PB
+    double* W = P + n * PB;   // (run) x PB, row a at W + a * PB
+    for (int p0 = q; p0 < end; p0 += PB) {
+        const int pb = min(PB, end - p0), prev = p0 - q;
+        for (int e = tid; e < n * PB; e += nt) {
+            const int t = e / PB, j = e % PB;
+            P[e] = (j < pb) ? Z[(int64_t)t * nvec + p0 + j] : 0.0;
+        }
+        __syncthreads();
+        for (int pass = 0; pass < 2 && prev > 0; ++pass) {
+            // W[a][j] = sum_t Z[t][q + a] P[t][j]: thread per earlier member a
+            for (int a = tid; a < prev; a += nt) {
+                double acc[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+                const double* zc = Z + q + a;
+                for (int t = 0; t < n; ++t) {
+                    const double z = zc[(int64_t)t * nvec];
+                    const double* pr = P + t * PB;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < PB) acc[j] = fma(z, pr[j], acc[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < PB) W[a * PB + j] = acc[j];
+            }
+            __syncthreads();
+            // P[t][j] -= sum_a Z[t][q + a] W[a][j]: thread per row t
+            for (int t = tid; t < n; t += nt) {
+                double acc[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = (j < PB) ? P[t * PB + j] : 0.0;
+                const double* zr = Z + (int64_t)t * nvec + q;
+                for (int a = 0; a < prev; ++a) {
+                    const double z = zr[a];
+                    const double* wr = W + a * PB;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < PB) acc[j] = fma(-z, wr[j], acc[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < PB) P[t * PB + j] = acc[j];
+            }
+            __syncthreads();
+        }
+        // CGS2 inside the panel (shared memory)
+        for (int j = 0; j < pb; ++j) {
+            for (int pass = 0; pass < 2 && j > 0; ++pass) {
+                for (int i = warp; i < j; i += nw) {  // d_i = P[:, i] . P[:, j]
+                    double d = 0.0;
+                    for (int t = lane; t < n; t += 32) d = fma(P[t * PB + i], P[t * PB + j], d);
+                    d = warp_sum_d(d);
+                    if (lane == 0) red[i] = d;
+                }
+                __syncthreads();
+                for (int t = tid; t < n; t += nt) {
+                    double acc = P[t * PB + j];
+                    for (int i = 0; i < j; ++i) acc = fma(-red[i], P[t * PB + i], acc);
+                    P[t * PB + j] = acc;
+                }
+                __syncthreads();
+            }
+            double nr = 0.0;
+            for (int t = tid; t < n; t += nt) nr = fma(P[t * PB + j], P[t * PB + j], nr);
+            nr = block_sum_d(nr, red + 32);
+            const double sc = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+            for (int t = tid; t < n; t += nt) P[t * PB + j] *= sc;
+            __syncthreads();
+        }
+        for (int e = tid; e < n * PB; e += nt) {
+            const int t = e / PB, j = e % PB;
+            if (j < pb) Z[(int64_t)t * nvec + p0 + j] = P[e];
+        }
+        __syncthreads();
+    }
+}
 __global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const double* __restrict__ wdesc,
                                                       const double* __restrict__ bounds, double* __restrict__ Z) {
     __shared__ double red[64];
@@ -1276,6 +1372,10 @@ __global__ void __launch_bounds__(256) k_cluster_orth(int n, int nvec, const dou
     // these directions by sqrt(lambda) or cuts them at its rank threshold
     if (fabs(wdesc[q]) <= 1e-10 * bounds[3]) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (end - q > kPanelMin && n <= kPanelMaxN && end - q <= min(kPanelMaxRun, n)) {
+        cluster_orth_panels(n, nvec, q, end, Z, dots, red);
+        return;
+    }
     for (int i = q + 1; i < end; ++i) {
         for (int pass = 0; pass < 2; ++pass) {
             for (int p = q + warp; p < i; p += 8) {
@@ -1440,7 +1540,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
                                        (int)(2 * sizeof(double) * kEighLargeMax)));
         AERO_CUDA(cudaFuncSetAttribute(k_twisted, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
         AERO_CUDA(cudaFuncSetAttribute(k_cluster_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * kEighLargeMax)));
+                                       (int)std::max({sizeof(double) * kEighLargeMax, cluster_orth_smem(256), cluster_orth_smem(kPanelMaxN)})));
         AERO_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(sizeof(double) * (BT_NB * BT_NB + BT_NB * (BT_NB - 1) / 2))));
         int sms = 0;
@@ -1601,7 +1701,7 @@ void eigh_large(cudaStream_t st, int n, double* A, int lda, double* w, int nvec)
     }
     AERO_LAUNCHED();
     note_launch();
-    k_cluster_orth<<<nvec, 256, sizeof(double) * (size_t)n, st>>>(n, nvec, w, bounds, wk.Z.p);
+    k_cluster_orth<<<nvec, 256, cluster_orth_smem(n), st>>>(n, nvec, w, bounds, wk.Z.p);
     AERO_LAUNCHED();
     if (n <= 128) {  // direct reflector application + sign fix, warp per vector
         note_launch();
