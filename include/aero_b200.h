@@ -90,6 +90,10 @@ int aero_create(const aero_cfg* cfg, aero_sketch** out);
 int aero_destroy(aero_sketch* h);
 /* AeroState::set_theta (sketch.cpp:33-36) */
 int aero_set_theta(aero_sketch* h, double theta);
+/* performance hint, no semantic effect: `share` sketches run concurrently on
+ * this GPU (e.g. co-hosted distributed sites); their persistent cooperative
+ * iterate kernels then use at most 1/share of the resident CTAs each */
+int aero_set_grid_share(aero_sketch* h, int32_t share);
 /* Caller-owned random projections (north star: "projection
  * matrices passed in through the FFI"). The sketch consumes one RngState fork
  * per power_iteration (sketch.cpp:99, linalg.cpp:106-108: first r Gaussians)

@@ -109,6 +109,7 @@ SIGNATURES = [
     ("aero_destroy", i32, [vp]),
     ("aero_set_theta", i32, [vp, f64]),
     ("aero_set_rng_fill", i32, [vp, vp, vp]),
+    ("aero_set_grid_share", i32, [vp, i32]),
     ("aero_update_block", i32, [vp, P(f64), i64, i64, P(i64), P(f64), P(Event)]),
     ("aero_file_open", i32, [C.c_char_p, P(vp), P(i32), P(u64)]),
     ("aero_file_read", i32, [vp, P(f64), i64, P(i64)]),
@@ -415,6 +416,10 @@ class AeroState:
         out = np.empty((self.ell, self.d))
         _chk(lib().aero_query(self._h, lb, ub, _dp(out)))
         return out
+
+    def set_grid_share(self, share):
+        """Performance hint: `share` sketches run concurrently on this GPU."""
+        _chk(lib().aero_set_grid_share(self._h, int(share)))
 
     def update_from_file(self, path, t0=None, chunk_rows=16384, want_log=False):
         """Stream an AERO file through the sketch (streams.cpp:105-137 format):

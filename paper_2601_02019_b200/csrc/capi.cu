@@ -86,6 +86,11 @@ int aero_set_theta(aero_sketch* h, double theta) {
     REQ(h);
     return guard([&] { h->s->set_theta(theta); });
 }
+int aero_set_grid_share(aero_sketch* h, int32_t share) {
+    REQ(h);
+    h->s->set_grid_share(share);
+    return AERO_OK;
+}
 int aero_set_rng_fill(aero_sketch* h, aero_rng_fill fn, void* ctx) {
     REQ(h);
     return guard([&] { h->s->set_rng_source(h->s->host_rng_default(), fn, ctx); });

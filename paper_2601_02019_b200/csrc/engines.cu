@@ -49,6 +49,9 @@ MlEngine::MlEngine(int d, int64_t n, double r_max, double eps, uint64_t seed, ui
         heavy_.emplace_back();
         lq_.emplace_back();
     }
+    // the levels ingest concurrently: their cooperative iterate launches must
+    // co-reside instead of serializing on the whole GPU
+    for (auto& l : levels_) l->set_grid_share(levels());
 }
 
 int64_t MlEngine::combined_len(int j) const {

@@ -1379,6 +1379,246 @@ __global__ void __launch_bounds__(32 * kWarpIterWarps) k_iterate_warp(
     }
 }
 
+// Medium buffers (96 < R <= 512; the C3 levels, the C4 sites): a CTA of
+// kCtaIterWarps warps runs its jobs (one per warp, k <= 2) through ALL their
+// phases with no grid barrier. G (R x R, L2-resident) is streamed once per
+// phase per CTA through shared memory in kCtaIterLB-column chunks and shared
+// by the CTA's warps; iterates live in registers (lanes over rows). Same
+// arithmetic and summation order as k_iterate_warp. The grid-wide persistent
+// kernel spends ~26 us per phase on barriers and latency at these sizes.
+constexpr int kCtaIterWarps = 4;
+constexpr int kCtaIterLB = 32;
+constexpr int kCtaIterMaxR = 512;
+template <int RT>
+__global__ void __launch_bounds__(32 * kCtaIterWarps) k_iterate_cta(
+    const IterJob* __restrict__ jobs, int njobs, const double* __restrict__ G, int ldg, int R,
+    double* __restrict__ X, int ldx, double* __restrict__ H, int* __restrict__ status,
+    double* __restrict__ out_sig, double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped) {
+    extern __shared__ double smc[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ int s_r[kCtaIterWarps], s_np[kCtaIterWarps];
+    const int j = blockIdx.x * kCtaIterWarps + warp;
+    IterJob jb{};
+    bool alive = false;
+    if (j < njobs) {
+        jb = jobs[j];
+        alive = status[j] == JOB_ACTIVE;
+        if (!alive && lane < jb.k) out_sig[jb.col + lane] = 0.0;
+    }
+    if (lane == 0) {
+        s_r[warp] = alive ? jb.r : 0;
+        s_np[warp] = alive ? jb.nphase : 0;
+    }
+    __syncthreads();
+    int rmax = 0, pmax = 0;
+#pragma unroll
+    for (int w = 0; w < kCtaIterWarps; ++w) {
+        rmax = max(rmax, s_r[w]);
+        pmax = max(pmax, s_np[w]);
+    }
+    double* sG = smc;                                                      // rmax x LB chunk
+    double* xs = smc + (size_t)R * kCtaIterLB + (size_t)warp * 2 * R;  // this warp's x
+    const int r = jb.r, k = jb.k;
+    double* xg = X + (int64_t)jb.col * ldx;
+    double x[RT][2], y[RT][2];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+        const int i = lane + 32 * t;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            x[t][a] = (alive && i < r && a < k) ? xg[i + (int64_t)a * ldx] : 0.0;
+            if (alive && i < R) xs[i + a * R] = x[t][a];
+        }
+    }
+    __syncwarp();
+    for (int p = 0; p < pmax; ++p) {
+        const bool act = alive && p < jb.nphase;
+        const bool last = (p == jb.nphase - 1);
+#pragma unroll
+        for (int t = 0; t < RT; ++t) y[t][0] = y[t][1] = 0.0;
+        // y = G x (rows < r): G streamed in column chunks shared by the warps
+        for (int l0 = 0; l0 < rmax; l0 += kCtaIterLB) {
+            const int lb = min(kCtaIterLB, rmax - l0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < rmax * lb; e += blockDim.x) {
+                const int ii = e % rmax, ll = e / rmax;
+                sG[ii + ll * rmax] = G[ii + (int64_t)(l0 + ll) * ldg];
+            }
+            __syncthreads();
+            if (act) {
+                const int le = min(lb, r - l0);
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int i = lane + 32 * t;
+                    if (i < r) {
+                        double y0 = y[t][0], y1 = y[t][1];
+                        for (int ll = 0; ll < le; ++ll) {
+                            const double g = sG[i + ll * rmax];
+                            y0 = fma(g, xs[l0 + ll], y0);
+                            y1 = fma(g, xs[l0 + ll + R], y1);
+                        }
+                        y[t][0] = y0;
+                        y[t][1] = y1;
+                    }
+                }
+            }
+        }
+        if (!act) continue;
+        if (k <= 1)
+#pragma unroll
+            for (int t = 0; t < RT; ++t) y[t][1] = 0.0;
+        if (jb.type == 0) {
+            if (!last) {
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t < RT; ++t) s = fma(y[t][0], y[t][0], s);
+                s = wsum(s);
+                const double nrm = sqrt(s);
+                if (nrm < 1e-300) {  // linalg.cpp:112-116
+                    if (lane == 0) status[j] = JOB_DEAD;
+                    alive = false;
+                    continue;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int i = lane + 32 * t;
+                    x[t][0] = (i < r) ? y[t][0] / nrm : 0.0;
+                    if (i < R) xs[i] = x[t][0];
+                }
+                __syncwarp();
+            } else {
+                double s = 0.0;  // sigma1^2 = x^T G x (linalg.cpp:119)
+#pragma unroll
+                for (int t = 0; t < RT; ++t) s = fma(x[t][0], y[t][0], s);
+                s = wsum(s);
+                if (lane == 0) out_sig[jb.col] = s;
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int i = lane + 32 * t;
+                    if (i < r) xg[i] = x[t][0];
+                }
+            }
+            continue;
+        }
+        // simul: S = X^T Y, T = S^{-1/2} (closed-form 2x2 / scalar), clamp
+        double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            s00 = fma(x[t][0], y[t][0], s00);
+            s01 = fma(x[t][0], y[t][1], s01);
+            s10 = fma(x[t][1], y[t][0], s10);
+            s11 = fma(x[t][1], y[t][1], s11);
+        }
+        s00 = wsum(s00);
+        s01 = wsum(s01);
+        s10 = wsum(s10);
+        s11 = wsum(s11);
+        double Tm[4], l0, l1;
+        if (k == 1) {
+            l0 = s00;
+            l1 = 0.0;
+            Tm[0] = 1.0;
+            Tm[1] = Tm[2] = 0.0;
+            Tm[3] = 1.0;
+        } else {
+            eig2_closed(s00, 0.5 * (s01 + s10), s11, l0, l1, Tm);
+        }
+        const double lmax = (k == 1) ? fmax(l0, 0.0) : fmax(fmax(l0, l1), 0.0);
+        const bool ok0 = l0 > 0.0 && l0 > 1e-14 * lmax, ok1 = (k > 1) && l1 > 0.0 && l1 > 1e-14 * lmax;
+        const double i0 = ok0 ? 1.0 / sqrt(l0) : 0.0, i1 = ok1 ? 1.0 / sqrt(l1) : 0.0;
+        if (last && out_clamped && lane == 0) out_clamped[j] = (!ok0) + (k > 1 && !ok1);
+        Tm[0] *= i0;
+        Tm[1] *= i0;
+        Tm[2] *= i1;
+        Tm[3] *= i1;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int i = lane + 32 * t;
+            const double h0 = fma(x[t][0], Tm[0], (k > 1) ? x[t][1] * Tm[1] : 0.0);
+            const double h1 = fma(x[t][0], Tm[2], (k > 1) ? x[t][1] * Tm[3] : 0.0);
+            const double n0 = fma(y[t][0], Tm[0], (k > 1) ? y[t][1] * Tm[1] : 0.0);
+            const double n1 = fma(y[t][0], Tm[2], (k > 1) ? y[t][1] * Tm[3] : 0.0);
+            if (last && i < r) {
+                H[i + (int64_t)jb.col * ldx] = h0;
+                if (k > 1) H[i + (int64_t)(jb.col + 1) * ldx] = h1;
+            }
+            x[t][0] = (i < r) ? n0 : 0.0;
+            x[t][1] = (i < r && k > 1) ? n1 : 0.0;
+            if (i < R) {
+                xs[i] = x[t][0];
+                xs[i + R] = x[t][1];
+            }
+        }
+        __syncwarp();
+        if (!last) continue;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const int i = lane + 32 * t;
+            if (i < r) {
+                xg[i] = x[t][0];
+                if (k > 1) xg[i + ldx] = x[t][1];
+            }
+        }
+        // Ritz values: eig(X^T X) (linalg.cpp:145-150), sorted descending, sign-fixed
+        double w00 = 0.0, w01 = 0.0, w11 = 0.0;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            w00 = fma(x[t][0], x[t][0], w00);
+            w01 = fma(x[t][0], x[t][1], w01);
+            w11 = fma(x[t][1], x[t][1], w11);
+        }
+        w00 = wsum(w00);
+        w01 = wsum(w01);
+        w11 = wsum(w11);
+        if (lane == 0) {
+            double* vr = out_vr + (int64_t)jb.col * kv;
+            if (k == 1) {
+                out_sig[jb.col] = sqrt(fmax(w00, 0.0));
+                vr[0] = 1.0;
+            } else {
+                double V2[4], a0, a1;
+                eig2_closed(w00, w01, w11, a0, a1, V2);
+                const int r0 = (a1 > a0) ? 1 : 0, r1 = (a0 >= a1) ? 1 : 0;
+                const double lam[2] = {a0, a1};
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int rk = (cc == 0) ? r0 : r1;
+                    const double v0 = V2[2 * cc], v1 = V2[2 * cc + 1];
+                    const int at = (fabs(v1) > fabs(v0)) ? 1 : 0;
+                    const double sg = ((at ? v1 : v0) < 0.0) ? -1.0 : 1.0;
+                    vr[0 + rk * 2] = sg * v0;
+                    vr[1 + rk * 2] = sg * v1;
+                    out_sig[jb.col + rk] = sqrt(fmax(lam[cc], 0.0));
+                }
+            }
+        }
+    }
+}
+
+bool iterate_cta(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
+                 int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
+                 int max_k) {
+    if (R > kCtaIterMaxR || max_k > 2 || njobs <= 0) return false;
+    const size_t smem = sizeof(double) * ((size_t)R * kCtaIterLB + (size_t)kCtaIterWarps * 2 * R);
+    static bool attr = false;
+    if (!attr) {
+        const int mx = (int)(sizeof(double) * ((size_t)kCtaIterMaxR * kCtaIterLB + (size_t)kCtaIterWarps * 2 * kCtaIterMaxR));
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate_cta<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        AERO_CUDA(cudaFuncSetAttribute(k_iterate_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        attr = true;
+    }
+    const int grid = (njobs + kCtaIterWarps - 1) / kCtaIterWarps;
+    if (R <= 256)
+        k_iterate_cta<8><<<grid, 32 * kCtaIterWarps, smem, st>>>(jobs, njobs, G, ldg, R, X, ldx, H, status, out_sig,
+                                                                 out_vr, kv, out_clamped);
+    else
+        k_iterate_cta<16><<<grid, 32 * kCtaIterWarps, smem, st>>>(jobs, njobs, G, ldg, R, X, ldx, H, status,
+                                                                  out_sig, out_vr, kv, out_clamped);
+    AERO_LAUNCHED();
+    return true;
+}
+
 bool iterate_warp(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
                   int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
                   int max_k) {

@@ -127,6 +127,10 @@ void iterate_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int max
 bool iterate_warp(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
                   int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
                   int max_k);
+// 96 < R <= 512, k <= 2: one CTA per 4 jobs, all phases, G streamed through shared memory
+bool iterate_cta(cudaStream_t st, const IterJob* jobs, int njobs, const double* G, int ldg, int R, double* X,
+                 int ldx, double* H, int* status, double* out_sig, double* out_vr, int kv, int* out_clamped,
+                 int max_k);
 
 // ---- small dense helpers ---------------------------------------------------
 // symmetric eigendecomposition of `batch` n x n matrices (column-major, ld,

@@ -301,15 +301,24 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
     double big = 0.0;
     for (int j = 0; j < njobs; ++j) big = std::max(big, (double)jobs_h_[j].r);
     const bool small_phases = big * big * (double)ncol_total < 1e8;
-    if (persistent_ && R <= 96 && max_k <= 2) {
-        // small buffer: one warp per job, all phases, G in shared memory
+    // experimental (AERO_CTA_ITER=1): measured slower than the persistent
+    // grid kernel at C3/C4 (G chunk loads are not yet double-buffered)
+    static const bool use_cta = getenv("AERO_CTA_ITER") != nullptr;
+    const bool cta_iter = persistent_ && use_cta && R > 96 && R <= 512 && max_k <= 2 && !(i8_ && R >= i8_min_rows_);
+    if (persistent_ && ((R <= 96 && max_k <= 2) || cta_iter)) {
+        // small buffer: one warp per job, all phases, G in shared memory;
+        // medium buffer (<= 512): 4 jobs per CTA, G streamed through shared memory
         double flops = 0.0;
         for (int j = 0; j < njobs; ++j) flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k * jobs_h_[j].nphase;
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(0), st_));
         iter_init(st_, jobs_d_, njobs, G_.p, cap_, X_.p, ldx_, R, status_d_, panel_d_);
         if (profiling) AERO_CUDA(cudaEventRecord(ev_at(2), st_));
-        iterate_warp(st_, jobs_d_, njobs, G_.p, cap_, R, X_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p, kv_, clamp_d_,
-                     max_k);
+        if (R <= 96)
+            iterate_warp(st_, jobs_d_, njobs, G_.p, cap_, R, X_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p, kv_,
+                         clamp_d_, max_k);
+        else
+            iterate_cta(st_, jobs_d_, njobs, G_.p, cap_, R, X_.p, ldx_, H_.p, status_d_, sig_.p, vr_.p, kv_,
+                        clamp_d_, max_k);
         if (profiling) {
             AERO_CUDA(cudaEventRecord(ev_at(3), st_));
             prof.product_launches++;
@@ -359,7 +368,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
             max_tiles = std::max(max_tiles, ((ncol + 63) / 64) * ((R + 127) / 128));
         }
         // CTAs: one per job for the normalizations, ~8 K-splits per product tile
-        const int grid = std::min(iterate_grid(R), std::max({njobs, 8 * max_tiles, 16}));
+        const int grid = std::min(std::max(16, iterate_grid(R) / grid_share_), std::max({njobs, 8 * max_tiles, 16}));
         double flops = 0.0;
         for (int p = 0; p < maxphase; ++p) {
             int ncol = 0;

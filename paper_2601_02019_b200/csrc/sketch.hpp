@@ -47,6 +47,10 @@ class Sketch {
     Sketch& operator=(const Sketch&) = delete;
 
     void set_theta(double th);
+    // sketches sharing one GPU concurrently (MlState levels, co-hosted sites):
+    // cooperative iterate launches use at most 1/share of the resident CTAs so
+    // that the sharers' persistent kernels co-run instead of serializing
+    void set_grid_share(int share) { grid_share_ = share < 1 ? 1 : share; }
     // rows: host or device pointer (row-major, ld); n sequential updates
     // amplified: n sequential update_amplified calls (sketch.cpp:45-48); an
     // AttpState built with delta always amplifies (attp.hpp:24)
@@ -136,6 +140,7 @@ class Sketch {
     bool host_prof_ = getenv("AERO_HOST_PROF") != nullptr;  // dev instrumentation
     double prof_append_ms_ = 0.0, prof_iter_ms_ = 0.0;
     int cfg_max_batch_ = 0;  // caller-set batch cap (0 = engine default)
+    int grid_share_ = 1;
     int64_t clock_ = 0, last_dump_t_ = 0;
     uint64_t forks_ = 0;
     int r_ = 0;

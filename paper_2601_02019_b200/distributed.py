@@ -88,6 +88,9 @@ class DistributedSketch:
         self.exchange = ThresholdExchange(m, eps, rank, world, group, latency, self.window)
         self.sites = {j: AeroState(d, eps, 0.0, seed=seed, stream=SKETCH_STREAM_BASE + j, device=device)
                       for j in self.exchange.local}
+        if len(self.sites) > 1:  # co-hosted sites run concurrently: share the GPU's CTAs
+            for s in self.sites.values():
+                s.set_grid_share(len(self.sites))
         self.ell = next(iter(self.sites.values())).ell if self.sites else int(np.ceil(2.0 / eps))
         self._comm = None
         if use_nccl is None:
