@@ -368,7 +368,11 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
             max_tiles = std::max(max_tiles, ((ncol + 63) / 64) * ((R + 127) / 128));
         }
         // CTAs: one per job for the normalizations, ~8 K-splits per product tile
-        const int grid = std::min(std::max(16, iterate_grid(R) / grid_share_), std::max({njobs, 8 * max_tiles, 16}));
+        // the split-K factors (hence every summation order, hence every
+        // decision) follow the unshared grid; the launch may use fewer CTAs
+        // (grid share: concurrent sketches), which then loop over the items
+        const int grid_full = std::min(iterate_grid(R), std::max({njobs, 8 * max_tiles, 16}));
+        const int grid = std::min(grid_full, std::max(16, iterate_grid(R) / grid_share_));
         double flops = 0.0;
         for (int p = 0; p < maxphase; ++p) {
             int ncol = 0;
@@ -378,7 +382,7 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
                     flops += 2.0 * jobs_h_[j].r * (double)jobs_h_[j].r * jobs_h_[j].k;
                 }
             const int tiles = ((ncol + 63) / 64) * ((R + 127) / 128);
-            int splits = std::max(1, std::min({grid / std::max(tiles, 1), 16, std::max(1, kt / 2)}));
+            int splits = std::max(1, std::min({grid_full / std::max(tiles, 1), 16, std::max(1, kt / 2)}));
             while (splits > 1 && (size_t)splits * R * ncol > ws_.n) --splits;
             phase_h_[p] = std::max(ncol, 1);
             phase_h_[kMaxPhases + p] = splits;
