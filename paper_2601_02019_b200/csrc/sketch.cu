@@ -1008,7 +1008,7 @@ void Sketch::ensure_query_buffers() {
 
 void Sketch::accumulate_residual(double* B, double beta_first) {
     if (r_ > 0)
-        dgemm(st_, false, true, d_, d_, r_, 1.0, C_.p, d_, C_.p, d_, beta_first, B, d_);
+        gemm_acc(st_, false, true, d_, d_, r_, 1.0, C_.p, d_, C_.p, d_, beta_first, B, d_, ws_.p, ws_.n);
     else if (beta_first == 0.0)
         fill_zero(st_, B, (int64_t)d_ * d_);
 }
@@ -1032,8 +1032,9 @@ void Sketch::accumulate_restore(double* B, int64_t first, int64_t last) {
         }
         const double* Z = ch->z + (size_t)c0 * d_;
         const double* Mt = ch->mt + (size_t)c0 * d_;
-        dgemm(st_, false, true, d_, d_, cols, 1.0, Z, d_, Mt, d_, 1.0, B, d_);  // Z M
-        dgemm(st_, false, true, d_, d_, cols, 1.0, Mt, d_, Z, d_, 1.0, B, d_);  // (Z M)^T
+        // the d x d restore products on the fp64 DMMA engine (split-K, fixed order)
+        gemm_acc(st_, false, true, d_, d_, cols, 1.0, Z, d_, Mt, d_, 1.0, B, d_, ws_.p, ws_.n);   // Z M
+        gemm_acc(st_, false, true, d_, d_, cols, 1.0, Mt, d_, Z, d_, 1.0, B, d_, ws_.p, ws_.n);   // (Z M)^T
         qy_.alloc((size_t)d_ * ch->cap + 2 * (size_t)ch->cap + 64);
         double* Yk = qy_.p;
         // per-snapshot K terms (batched kernel for xi <= 64, GEMMs otherwise)
@@ -1062,7 +1063,7 @@ void Sketch::accumulate_restore(double* B, int64_t first, int64_t last) {
             AERO_CUDA(cudaFreeAsync(dso, st_));
             AERO_CUDA(cudaStreamSynchronize(st_));
         }
-        dgemm(st_, false, true, d_, d_, cols, -1.0, Yk + (size_t)c0 * d_, d_, Z, d_, 1.0, B, d_);
+        gemm_acc(st_, false, true, d_, d_, cols, -1.0, Yk + (size_t)c0 * d_, d_, Z, d_, 1.0, B, d_, ws_.p, ws_.n);
         i = j;
     }
 }

@@ -60,10 +60,12 @@ def run_attp(cfg, n, probe, chunk):
         mass += float((rows * rows).sum())
         t = t0 + m
         if t % probe == 0 or t == n:
+            q0 = time.perf_counter()
             b = torch.from_numpy(s.query(t)).to(DEV)
+            q_ms = (time.perf_counter() - q0) * 1e3
             err = spec_sym(g - b.T @ b) / mass
-            out.append({"t": t, "err": err})
-            print(f"t={t} err={err:.5g} ({t / t_upd:.0f} rows/s)", flush=True)
+            out.append({"t": t, "err": err, "query_ms": q_ms, "snaps": int(s.info().snaps)})
+            print(f"t={t} err={err:.5g} ({t / t_upd:.0f} rows/s) query {q_ms:.0f} ms", flush=True)
     inf = s.info()
     return out, {"rows_per_s_update": n / t_upd, "snap_cols": int(inf.snap_cols), "snaps": int(inf.snaps)}
 
