@@ -592,7 +592,7 @@ def main():
         traffic = None
         i8 = info.ell * 2 >= 1024 and os.environ.get("AERO_PRODUCT_I8", "1") != "0"
         kern = ("k_iterate_i8 (persistent cooperative: every phase of a batch = G.X on the int8 tcgen05 tensor "
-                "cores by exact 7-slice Ozaki splitting, TMEM accumulators, + per-job normalization; kernels.cu, "
+                "cores by 6-slice balanced-digit Ozaki splitting, TMEM accumulators, + per-job normalization; kernels.cu, "
                 "ozaki.cuh); fp64-equivalent useful product flops (2 r^2 k per job per phase) over the whole kernel "
                 "time, against the fp64 DGEMM peak the same products would have on the DMMA pipe") if i8 else (
                 "k_iterate (persistent: split-K DMMA G.X products of every phase of a batch + per-job "
@@ -604,7 +604,7 @@ def main():
                     "product_share_of_step": prof["product_ms"] / ms_p,
                     "flops_per_launch": prof["product_flops"] / max(1, prof["product_launches"]),
                     "ms_per_launch": prof["product_ms"] / max(1, prof["product_launches"])}
-        if i8:  # the same kernel against the pipe it runs on: 28 int8 MMA slice pairs per fp64 product
+        if i8:  # the same kernel against the pipe it runs on: 21 int8 MMA slice pairs per fp64 product
             bf16 = None
             try:
                 mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -612,8 +612,8 @@ def main():
             except Exception:
                 pass
             i8_peak = 2.0 * bf16 if bf16 else 4500.0
-            roofline["int8_pipe"] = {"achieved_tops": achieved * 28, "peak_tops": i8_peak,
-                                     "frac": achieved * 28 / i8_peak,
+            roofline["int8_pipe"] = {"achieved_tops": achieved * 21, "peak_tops": i8_peak,
+                                     "frac": achieved * 21 / i8_peak,
                                      "peak_source": ("2 x measured dense bf16 (MEASURED_PEAKS.json)" if bf16
                                                      else "nominal B200 dense int8 4.5 POP/s")}
         f_row = reference_literal_flops(ev, d, info.ell)

@@ -550,7 +550,8 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                               int* __restrict__ status, double* __restrict__ out_sig,
                               double* __restrict__ out_vr, int kv, int* __restrict__ out_clamped,
                               const double* __restrict__ ws, int wsM, int64_t sstride, int splits,
-                              double* sm, const OzSliceDst xs = OzSliceDst{}) {
+                              double* sm, const OzSliceDst xs = OzSliceDst{}, const OzBulkWs bw = OzBulkWs{},
+                              unsigned* bw_use = nullptr) {
     if (phase >= jb.nphase) return;
     const int st = status[jidx];
     const bool last = (phase == jb.nphase - 1);
@@ -582,10 +583,39 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
     const double* y;
     int ldy;
     if (WS) {
+        const int tot = r * k;
+        const int re = (r + 1) & ~1;  // 16-byte multiple per column copy
+        const bool bulk = bw.buf && (size_t)splits * k * re <= bw.cap && !(wsM & 1) && !(sstride & 1);
+        if (bulk) {
+            // the job's split-K partials (k columns x splits) pulled into shared
+            // memory by bulk copies (async proxy: all in flight at once, no
+            // per-thread load queue), then summed in the same fixed order
+            if (tid == 0) {
+                mbar_expect_tx(bw.bar, (unsigned)(splits * k * re) * 8u);
+                for (int z = 0; z < splits; ++z)
+                    for (int a = 0; a < k; ++a)
+                        bulk_g2s(smem_u32(bw.buf + (size_t)(z * k + a) * re),
+                                 ws + z * sstride + (int64_t)(jb.col + a) * wsM, (unsigned)re * 8u, bw.bar);
+            }
+            mbar_wait(bw.bar, *bw_use & 1u);
+            ++*bw_use;
+            if (st == JOB_ACTIVE)
+                for (int a = 0; a < k; ++a)
+                    for (int i = tid; i < r; i += nt) {
+                        double v = 0.0;
+                        for (int z = 0; z < splits; z += 4) {
+                            double t[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                t[q] = (z + q < splits) ? bw.buf[(size_t)((z + q) * k + a) * re + i] : 0.0;
+                            v += (t[0] + t[1]) + (t[2] + t[3]);
+                        }
+                        ysh[i + a * r] = v;
+                    }
+        } else {
         // fixed-order split-K sum; 8 entries x 4 splits of loads in flight per
         // thread (a plain per-entry loop serializes one L2 round trip per split)
         constexpr int U = 8;
-        const int tot = r * k;
         for (int e0 = tid; e0 < tot; e0 += U * nt) {
             const double* pp[U];
             bool ok[U];
@@ -610,6 +640,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (ok[u]) ysh[e0 + u * nt] = v[u];
+        }
         }
         __syncthreads();
         NJ_MARK(0);
@@ -991,6 +1022,8 @@ struct IterI8Args {
     int8_t* xb;
     int* xfe;
     unsigned long long* prof;  // optional (AERO_I8_PROF): CTA 0 ns per segment
+    int smem_bytes;            // dynamic shared memory of the launch
+    int bulk_ws;               // split-K partials by bulk copy into shared memory (A/B: AERO_BULK_WS=0)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1005,11 +1038,16 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
     uint8_t* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
     double* smd = reinterpret_cast<double*>(sm);
     __shared__ uint32_t slot;
+    __shared__ __align__(8) uint64_t wsbar;  // split-K partials landed in shared memory (normalize_job)
     constexpr int S = kOzSlices;
     if ((threadIdx.x >> 5) == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&slot)),
                      "r"(OzCfg<S>::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&wsbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -1018,6 +1056,12 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
     unsigned epoch = 0;
     const unsigned G = gridDim.x;
     const int R = a.R, nkb_all = a.Kp / kOzBK, tm = a.Rp / kOzBM;
+    const int Rld = (R + 1) & ~1;  // partial columns start 16-byte aligned (bulk copies)
+    // shared memory past the normalization scratch receives a job's partials
+    const size_t nd = (normalize_smem_doubles<KM>(R, true) + 1) & ~(size_t)1;
+    const size_t smd_total = ((size_t)a.smem_bytes - (size_t)(sm - smraw)) / sizeof(double);
+    const OzBulkWs bw{a.bulk_ws && smd_total > nd ? smd + nd : nullptr, &wsbar, smd_total > nd ? smd_total - nd : 0};
+    unsigned bw_use = 0;
     {  // X slices for phase 0
         const int ncol0 = a.phase_ncol[0], np0 = (ncol0 + kOzBN - 1) / kOzBN * kOzBN;
         for (int c = blockIdx.x; c < np0; c += G) {
@@ -1038,15 +1082,20 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
         tp = t_;                                \
     }
     for (int p = 0; p < a.maxphase; ++p) {
-        const int ncol = a.phase_ncol[p], splits = a.phase_splits[p];
+        // phase_splits[p] = split-K factor | effective slices << 16 (0: all S)
+        const int ncol = a.phase_ncol[p], splits = a.phase_splits[p] & 0xffff, se = a.phase_splits[p] >> 16;
         const int tn = (ncol + kOzBN - 1) / kOzBN, per = (nkb_all + splits - 1) / splits;
         const int items = tn * tm * splits;
-        const int64_t sstride = (int64_t)R * ncol;
+        const int64_t sstride = (int64_t)Rld * ncol;
         for (int it = blockIdx.x; it < items; it += G) {
             const int z = it / (tn * tm), rem = it % (tn * tm);
             const int kb0 = z * per, nkb = max(0, min(nkb_all - kb0, per));
-            ozaki_tile<S>(R, ncol, nkb_all, rem / tn, rem % tn, kb0, nkb, a.ga, a.xb, a.gea, a.xfe,
-                          a.ws + z * sstride, R, nullptr, 0, sm, tmem);
+            if (se == S - 1)
+                ozaki_tile<S, S - 1>(R, ncol, nkb_all, rem / tn, rem % tn, kb0, nkb, a.ga, a.xb, a.gea, a.xfe,
+                                     a.ws + z * sstride, Rld, nullptr, 0, sm, tmem);
+            else
+                ozaki_tile<S>(R, ncol, nkb_all, rem / tn, rem % tn, kb0, nkb, a.ga, a.xb, a.gea, a.xfe,
+                              a.ws + z * sstride, Rld, nullptr, 0, sm, tmem);
         }
         I8_MARK(0);
         grid_sync_async(a.bar, epoch, G);
@@ -1056,7 +1105,8 @@ __global__ void __launch_bounds__(256, 1) k_iterate_i8(IterI8Args a) {
             __syncthreads();
             // the normalization also slices the new iterate for the next product
             normalize_job<KM, true>(jb, j, p, a.X, nullptr, a.ldx, a.H, a.status, a.out_sig, a.out_vr, a.kv,
-                                    a.out_clamped, a.ws, R, sstride, splits, smd, OzSliceDst{a.xb, a.xfe, a.Kp});
+                                    a.out_clamped, a.ws, Rld, sstride, splits, smd, OzSliceDst{a.xb, a.xfe, a.Kp},
+                                    bw, &bw_use);
             __syncthreads();
             if (j == 0) I8_MARK(4);
         }
@@ -1083,7 +1133,7 @@ int ozaki_splits(const OzakiGram& oz, int N, size_t ws_doubles) {
     }
     const int tm = oz.Rp / kOzBM, tn = (N + kOzBN - 1) / kOzBN, nkb = oz.Kp / kOzBK;
     int splits = std::max(1, std::min(sms / std::max(tm * tn, 1), nkb / 2));
-    while (splits > 1 && (size_t)splits * oz.R * N > ws_doubles) --splits;
+    while (splits > 1 && (size_t)splits * (oz.R + 1) * N > ws_doubles) --splits;  // padded leading dimension
     const int per = (nkb + splits - 1) / splits;
     return (nkb + per - 1) / per;
 }
@@ -1093,8 +1143,12 @@ void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int 
                            double* out_vr, int kv, int* out_clamped, double* ws, const int* phase_ncol,
                            const int* phase_splits, unsigned* bar, int max_k, int grid) {
     // the tile pipeline's stages or the normalization's scratch (phases are separate in time)
-    const size_t smem = std::max((size_t)OzCfg<kOzSlices>::SMEM,
-                                 sizeof(double) * normalize_smem_doubles<4>(R, true) + 1024 + 16);
+    // + room for one job's split-K partials (4 splits x max_k columns) when it fits
+    const size_t scratch = sizeof(double) * normalize_smem_doubles<4>(R, true) + 1024 + 16;
+    const size_t partials = sizeof(double) * 4 * (size_t)std::max(max_k, 2) * (size_t)(R + 2);
+    const size_t smem = std::max({(size_t)OzCfg<kOzSlices>::SMEM, scratch,
+                                  std::min(scratch + partials, (size_t)227 * 1024 - 4096)});
+    static const int bulk_ws = getenv("AERO_BULK_WS") ? atoi(getenv("AERO_BULK_WS")) : 1;
     static size_t attr = 0;
     if (attr < smem) {
         AERO_CUDA(cudaFuncSetAttribute(k_iterate_i8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1127,7 +1181,7 @@ void iterate_i8_persistent(cudaStream_t st, const IterJob* jobs, int njobs, int 
     }
     phases += (unsigned long long)maxphase;
     IterI8Args a{jobs, njobs, maxphase, R, ldx, kv, oz.Kp, oz.Rp, X, H, out_sig, out_vr, ws, status, out_clamped,
-                 colmask, phase_ncol, phase_splits, bar, oz.a, oz.ea, oz.b, oz.fb, prof};
+                 colmask, phase_ncol, phase_splits, bar, oz.a, oz.ea, oz.b, oz.fb, prof, (int)smem, bulk_ws};
     void* args[] = {&a};
     note_launch();
     AERO_CUDA(cudaLaunchCooperativeKernel(max_k <= 2 ? (void*)k_iterate_i8<2> : (void*)k_iterate_i8<4>, dim3(grid),

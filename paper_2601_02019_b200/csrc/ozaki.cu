@@ -9,16 +9,21 @@
 // fp64 DMMA pipe (k_product_mma, product.cu) peaks at ~35 TF/s on B200 while
 // the int8 tensor pipe peaks at ~4.5 POP/s.
 //
-// Scheme: every row i of G (and column c of X) is scaled by a power of two so
-// that its entries lie in (-1, 1) and is cut into S signed 7-bit slices:
-//     G_ik = 2^{e_i} sum_p a_p[i,k] 2^{-7(p+1)},  a_p in [-127, 127]
-// (exact: multiplications by powers of two and removals of integer parts).
-// Then  (G X)_ic = 2^{e_i + f_c - 14} sum_t 2^{-7t} D_t[i,c],
+// Scheme: every row i of G (and column c of X) gets a power-of-two bound
+// 2^{e_i} > max|G_i|, is rounded to F = 8S - 2 fractional bits below it and
+// written in S balanced signed base-256 digits (ozaki_slice.h):
+//     G_ik ~ 2^{e_i - F} sum_p a_p[i,k] 256^{S-1-p},  a_p in [-128, 127].
+// Then  (G X)_ic = 2^{e_i + f_c - 12} sum_t 2^{-8t} D_t[i,c],
 //       D_t = sum_{p+q=t} A_p B_q   (int8 x int8 -> int32, exact),
-// keeping the diagonals t < S. With S = 7 the dropped terms and the slice
-// remainders are below 2^-46 of max|G_i| max|X_c| per product term -- fp64
-// GEMM accuracy to within a small factor (tests/test_gpu_parity.py states the
-// tolerance and checks it against numpy fp64).
+// keeping the diagonals t < S: S(S+1)/2 = 21 slice-pair products at S = 6.
+// Error per product term, relative to 2^{e_i + f_c}: the two roundings
+// (2^-47 each) plus the dropped diagonals (t = 6: five pairs of at most
+// 128^2 2^-60) -- below 6.1 x 2^-46, i.e. below 2^-41 max|G_i| max|X_c| per
+// term in the worst case; the digits are balanced, so these terms carry random
+// signs and the observed error is two to three orders of magnitude smaller
+// (tests/test_gpu_parity.py states the bound and checks it against numpy
+// fp64). (Round 1 used 7-bit sign-magnitude slices: S = 7, 28 products, every
+// dropped term biased toward zero.)
 //
 // Kernel: CTA tile 128 (rows of G) x 64 (job columns), 256 threads. The
 // slicing kernels write every (tile, 64-byte K block) of all S slices as one

@@ -6,49 +6,24 @@
 #include <cstdint>
 
 #include "aero_common.cuh"
+#include "ozaki_slice.h"
 
 namespace aero_b200 {
 
-constexpr int kOzSlices = 7;  // 7-bit slices per fp64 value (49 bits)
+constexpr int kOzSlices = 6;  // balanced signed 8-bit slices per fp64 value (46 bits + sign, ozaki_slice.h)
 constexpr int kOzBK = 64;     // K bytes per tiled block (one pipeline stage)
 constexpr int kOzBM = 128;    // G-tile rows (UMMA M)
 constexpr int kOzBN = 64;     // X-tile columns (UMMA N)
 
-// cut 8 values (|x| < 2^e) into S signed 7-bit slices, packed 8 per uint64
+// cut 8 values (|x| < 2^e) into S balanced signed 8-bit slices, packed 8 per
+// uint64 (ozaki_slice.h)
 template <int S>
 __device__ __forceinline__ void ozaki_slice8(const double (&x)[8], int e, uint64_t (&pk)[S]) {
-#pragma unroll
-    for (int p = 0; p < S; ++p) pk[p] = 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        double y = scalbn(x[u], 7 - e);  // |y| < 128
-#pragma unroll
-        for (int p = 0; p < S; ++p) {
-            const double sv = trunc(y);
-            y = (y - sv) * 128.0;
-            pk[p] |= (uint64_t)(uint8_t)(int8_t)(int)sv << (8 * u);
-        }
-    }
+    ozaki_slice8_int<S>(x, e, pk);
 }
-
-// same bytes as ozaki_slice8, with the exact power-of-two scaling by one
-// multiply (|x| < 2^e, e far from the exponent limits) instead of scalbn
 template <int S>
 __device__ __forceinline__ void ozaki_slice8_pow2(const double (&x)[8], int e, uint64_t (&pk)[S]) {
-    const bool fast = e > -900 && e < 900;
-    const double sc = fast ? __longlong_as_double((long long)(1023 + 7 - e) << 52) : 0.0;
-#pragma unroll
-    for (int p = 0; p < S; ++p) pk[p] = 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        double y = fast ? x[u] * sc : scalbn(x[u], 7 - e);  // |y| < 128
-#pragma unroll
-        for (int p = 0; p < S; ++p) {
-            const double sv = trunc(y);
-            y = (y - sv) * 128.0;
-            pk[p] |= (uint64_t)(uint8_t)(int8_t)(int)sv << (8 * u);
-        }
-    }
+    ozaki_slice8_int<S>(x, e, pk);
 }
 
 template <int S, int TR, int NV>
@@ -122,20 +97,25 @@ struct OzSliceDst {
     int Kp = 0;
 };
 
+// Shared-memory landing zone of one job's split-K partials (normalize_job in
+// k_iterate_i8): buf holds cap doubles, bar is an mbarrier (count 1) reused
+// with alternating parity; buf == nullptr: partials are read with plain loads
+struct OzBulkWs {
+    double* buf = nullptr;
+    uint64_t* bar = nullptr;
+    size_t cap = 0;
+};
+
 // the S slices of one value x (|x| < 2^e) at K index k of vector i, as bytes
 // of the tiled image (TR vectors per tile)
 template <int S, int TR>
 __device__ __forceinline__ void ozaki_store_value(int8_t* __restrict__ out, int Kp, int i, int k, double x, int e) {
     const int nkb = Kp / kOzBK, t = i / TR, r = i % TR, b = k / kOzBK, kk = k % kOzBK, kc = kk >> 4;
     int8_t* base = out + ((int64_t)t * nkb + b) * S * TR * kOzBK + r * kOzBK + ((kc ^ ((r >> 1) & 3)) << 4) + (kk & 15);
-    // exact power-of-two scaling (|x| < 2^e, e far from the exponent limits)
-    double y = (e > -900 && e < 900) ? x * __longlong_as_double((long long)(1023 + 7 - e) << 52) : scalbn(x, 7 - e);
+    int8_t dg[S];
+    ozaki_slice1_int<S>(x, e, dg);
 #pragma unroll
-    for (int p = 0; p < S; ++p) {
-        const double sv = trunc(y);
-        y = (y - sv) * 128.0;
-        base[p * TR * kOzBK] = (int8_t)(int)sv;
-    }
+    for (int p = 0; p < S; ++p) base[p * TR * kOzBK] = dg[p];
 }
 
 // Slice vector i (v[0..lim), zero beyond; padded to Kp) into the product
@@ -244,16 +224,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
 // : M). `sm` is 1024-byte aligned shared memory of OzCfg<S>::SMEM - 1024
 // bytes, `tmem` an allocation of OzCfg<S>::TMEM_COLS columns; 256 threads.
 // Barriers are initialized here, so consecutive calls may reuse `sm`.
-template <int S>
+// SE <= S: only the leading SE slices of both images take part (diagonals
+// t < SE: SE(SE+1)/2 of the S(S+1)/2 slice-pair MMAs, SE/S of the bytes) -- a
+// product truncated to 8 SE - 2 bits, an opt-in experiment for the steering
+// phases of an iteration (AERO_OZ_SE; the default runs every phase at SE = S).
+template <int S, int SE = S>
 __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int tile_n, int kb0, int nkb,
                                   const int8_t* __restrict__ As, const int8_t* __restrict__ Bs,
                                   const int* __restrict__ ea, const int* __restrict__ fb, double* __restrict__ o,
                                   int ldo, const int* __restrict__ colmask, int direct, uint8_t* sm, uint32_t tmem) {
+    static_assert(SE >= 1 && SE <= S, "effective slices");
     using Cfg = OzCfg<S>;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * Cfg::STAGE);
     uint64_t* empty = full + 2;
     uint64_t* done = empty + 2;  // one commit after the last stage: accumulators final
-    double* cscale = reinterpret_cast<double*>(done + 2);  // kOzBN per-column 2^(f - 14)
+    double* cscale = reinterpret_cast<double*>(done + 2);  // kOzBN per-column 2^(f - 12)
     int* clim = reinterpret_cast<int*>(cscale + kOzBN);    // kOzBN per-column row limits
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int bm = tile_m * kOzBM, bn = tile_n * kOzBN;
@@ -268,7 +253,9 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
     }
     if (tid < kOzBN) {
         const int n = bn + tid;
-        cscale[tid] = (n < N) ? ldexp(1.0, fb[n] - 14) : 0.0;
+        // (G X)_ic = 2^(e_i + f_c - 2F) sum_pq d_p d'_q 256^(2(S-1) - p - q), F = 8S - 2:
+        // 2^(e_i + f_c - 12) sum_t 2^(-8t) D_t
+        cscale[tid] = (n < N) ? ldexp(1.0, fb[n] - 12) : 0.0;
         clim[tid] = (n >= N) ? 0 : ((direct && colmask) ? colmask[n] : M);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -280,9 +267,11 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
         const int8_t* Bblk = Bs + ((int64_t)tile_n * nkb_all + kb0) * Cfg::B_BYTES;
         auto load = [&](int st, int kb) {
             const uint32_t dA = sbase + st * Cfg::STAGE;
-            mbar_expect_tx(&full[st], Cfg::STAGE);
-            bulk_g2s(dA, Ablk + (int64_t)kb * Cfg::A_BYTES, Cfg::A_BYTES, &full[st]);
-            bulk_g2s(dA + Cfg::A_BYTES, Bblk + (int64_t)kb * Cfg::B_BYTES, Cfg::B_BYTES, &full[st]);
+            // slices are contiguous (p-major) inside a block: the leading SE of them
+            constexpr unsigned aB = SE * kOzBM * kOzBK, bB = SE * kOzBN * kOzBK;
+            mbar_expect_tx(&full[st], aB + bB);
+            bulk_g2s(dA, Ablk + (int64_t)kb * Cfg::A_BYTES, aB, &full[st]);
+            bulk_g2s(dA + Cfg::A_BYTES, Bblk + (int64_t)kb * Cfg::B_BYTES, bB, &full[st]);
         };
         load(0, 0);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -293,10 +282,10 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
 #pragma unroll
             for (int ks = 0; ks < kOzBK / 32; ++ks) {
 #pragma unroll
-                for (int p = 0; p < S; ++p) {
+                for (int p = 0; p < SE; ++p) {
                     const uint64_t da = umma_desc(aS + p * kOzBM * kOzBK + ks * 32);
 #pragma unroll
-                    for (int q = 0; q < S - p; ++q) {
+                    for (int q = 0; q < SE - p; ++q) {
                         const uint64_t db = umma_desc(bS + q * kOzBN * kOzBK + ks * 32);
                         mma_i8(tmem + (uint32_t)((p + q) * kOzBN), da, db, (kb > 0 || ks > 0 || p > 0) ? 1u : 0u);
                     }
@@ -331,15 +320,15 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.0;
         if (nkb > 0) {
-            uint32_t v[S][16];
+            uint32_t v[SE][16];
 #pragma unroll
-            for (int t = 0; t < S; ++t)
+            for (int t = 0; t < SE; ++t)
                 tmem_ld16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(t * kOzBN + c0), v[t]);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-            for (int t = S - 1; t >= 0; --t)  // Horner in 2^-7: sum_t 2^{-7t} D_t
+            for (int t = SE - 1; t >= 0; --t)  // Horner in 2^-8: sum_t 2^{-8t} D_t
 #pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] = fma(acc[j], 0x1.0p-7, (double)(int)v[t][j]);
+                for (int j = 0; j < 16; ++j) acc[j] = fma(acc[j], 0x1.0p-8, (double)(int)v[t][j]);
         }
         if (m < M) {
 #pragma unroll

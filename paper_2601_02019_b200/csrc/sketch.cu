@@ -339,7 +339,14 @@ void Sketch::run_iterate(int njobs, int R, int max_k) {
                 }
             ncol = std::max(ncol, 1);
             phase_h_[p] = ncol;
-            phase_h_[kMaxPhases + p] = ozaki_splits(oz_, ncol, ws_.n);
+            // effective slices of the phase's products (opt-in experiment, default
+            // all slices everywhere): the last oz_tail_ phases of every job run on
+            // all slices, the steering phases before them on oz_se_ (AERO_OZ_SE /
+            // AERO_OZ_TAIL)
+            int se = oz_se_;
+            for (int j = 0; j < njobs && se < ozaki_slices(); ++j)
+                if (jobs_h_[j].nphase > p && jobs_h_[j].nphase - 1 - p < oz_tail_) se = ozaki_slices();
+            phase_h_[kMaxPhases + p] = ozaki_splits(oz_, ncol, ws_.n) | (se << 16);
         }
         oz_.reserve_x(phase_h_[0]);
         AERO_CUDA(cudaMemcpyAsync(phase_d_, phase_h_, sizeof(int) * 2 * kMaxPhases, cudaMemcpyHostToDevice, st_));

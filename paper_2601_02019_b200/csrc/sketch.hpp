@@ -164,6 +164,10 @@ class Sketch {
     // buffer rows from which it is used (tools/product_i8_bench.py: at r = 1500,
     // n = 128..192 it beats DMMA); AERO_I8_MIN_ROWS overrides (tests force it on)
     int i8_min_rows_ = getenv("AERO_I8_MIN_ROWS") ? atoi(getenv("AERO_I8_MIN_ROWS")) : 1024;
+    // int8 iterate: slices used by the steering phases / full-precision tail phases per job
+    int oz_se_ = getenv("AERO_OZ_SE") ? std::min(ozaki_slices(), std::max(ozaki_slices() - 1, atoi(getenv("AERO_OZ_SE"))))
+                                      : ozaki_slices();
+    int oz_tail_ = getenv("AERO_OZ_TAIL") ? std::max(1, atoi(getenv("AERO_OZ_TAIL"))) : 3;
     OzakiGram oz_;
     RngPanels rng_;
     bool host_rng_default_ = false;  // AERO_FLAG_HOST_RNG

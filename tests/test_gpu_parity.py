@@ -682,11 +682,14 @@ def _product_ref(g, x, mask):
 
 @pytest.mark.parametrize("r,n", [(64, 1), (129, 3), (700, 64), (1500, 130), (2047, 192)])
 def test_int8_tensor_product_matches_fp64(r, n):
-    """ozaki.cu (tcgen05 kind::i8, 7 slices of 7 bits) vs numpy fp64.
-    Tolerance = the scheme's bound: row i of G and column c of X are cut
-    relative to their largest entries, so each product term is exact to
-    2^-46 max_k|G_ik| max_k|X_kc| and an entry to m_c 2^-44 max|G_i| max|X_c|
-    (m_c = the column's prefix length). The fp64 DMMA path is held to the fp64
+    """ozaki.cu (tcgen05 kind::i8, 6 balanced signed 8-bit slices, 21 slice-pair
+    MMAs) vs numpy fp64. Row i of G and column c of X are cut relative to their
+    largest entries; the scheme's worst-case bound is 6.1 x 2^-46 x 2^(e_i+f_c)
+    <= 2^-41 max_k|G_ik| max_k|X_kc| per product term (two roundings + the
+    dropped diagonals, ozaki.cu), i.e. m_c 2^-41 max|G_i| max|X_c| per entry
+    (m_c = the column's prefix length). Balanced digits give the dropped terms
+    random signs, so the kernel is held here to the 8x tighter m_c 2^-44 that
+    the round-1 7-bit sign-magnitude scheme guaranteed. The fp64 DMMA path is held to the fp64
     GEMM componentwise bound 1e-13 |G||X| (K u = 4.5e-13 at K = 2047).
     Masked rows are exactly 0 on both paths."""
     g, x, mask = _product_case(r, n, seed=r + n)
