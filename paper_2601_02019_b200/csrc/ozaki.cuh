@@ -137,7 +137,10 @@ struct OzCfg {
     static constexpr int A_BYTES = S * kOzBM * kOzBK;
     static constexpr int B_BYTES = S * kOzBN * kOzBK;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int SMEM = 2 * STAGE + 1024 + 128 + kOzBN * 12;  // + alignment slack, barriers, column scales
+    // pipeline stages: as many as fit beside the barriers (3 at S = 6: two
+    // bulk loads in flight behind the stage the tensor pipe is reading)
+    static constexpr int NST = (3 * STAGE + 2048 + kOzBN * 12 <= 225 * 1024) ? 3 : 2;
+    static constexpr int SMEM = NST * STAGE + 1024 + 128 + kOzBN * 12;  // + alignment slack, barriers, column scales
     static constexpr int TMEM_COLS = (S * kOzBN <= 256) ? 256 : 512;
 };
 
@@ -235,16 +238,17 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
                                   int ldo, const int* __restrict__ colmask, int direct, uint8_t* sm, uint32_t tmem) {
     static_assert(SE >= 1 && SE <= S, "effective slices");
     using Cfg = OzCfg<S>;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + 2 * Cfg::STAGE);
-    uint64_t* empty = full + 2;
-    uint64_t* done = empty + 2;  // one commit after the last stage: accumulators final
+    constexpr int NST = Cfg::NST;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * Cfg::STAGE);
+    uint64_t* empty = full + NST;
+    uint64_t* done = empty + NST;  // one commit after the last stage: accumulators final
     double* cscale = reinterpret_cast<double*>(done + 2);  // kOzBN per-column 2^(f - 12)
     int* clim = reinterpret_cast<int*>(cscale + kOzBN);    // kOzBN per-column row limits
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int bm = tile_m * kOzBM, bn = tile_n * kOzBN;
     __syncthreads();  // previous item (if any) is done with sm and TMEM
     if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NST; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], 1);
         }
@@ -273,10 +277,10 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
             bulk_g2s(dA, Ablk + (int64_t)kb * Cfg::A_BYTES, aB, &full[st]);
             bulk_g2s(dA + Cfg::A_BYTES, Bblk + (int64_t)kb * Cfg::B_BYTES, bB, &full[st]);
         };
-        load(0, 0);
+        for (int kb = 0; kb < NST - 1 && kb < nkb; ++kb) load(kb, kb);
         for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb & 1;
-            mbar_wait(&full[st], (kb >> 1) & 1);
+            const int st = kb % NST;
+            mbar_wait(&full[st], (kb / NST) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t aS = sbase + st * Cfg::STAGE, bS = aS + Cfg::A_BYTES;
 #pragma unroll
@@ -292,11 +296,14 @@ __device__ inline void ozaki_tile(int M, int N, int nkb_all, int tile_m, int til
                 }
             }
             umma_commit(&empty[st]);
-            // refill the other stage once the MMAs of kb-1 have drained it
-            // (those of kb are queued behind them, so the tensor pipe stays busy)
-            if (kb + 1 < nkb) {
-                if (kb >= 1) mbar_wait(&empty[st ^ 1], ((kb - 1) >> 1) & 1);
-                load(st ^ 1, kb + 1);
+            // refill the stage the MMAs of kb-1 have drained (those of kb are
+            // queued behind them, so the tensor pipe stays busy) with block
+            // kb + NST - 1: NST - 1 loads stay in flight
+            const int kn = kb + NST - 1;
+            if (kn < nkb) {
+                const int sn = kn % NST;  // == (kb - 1) % NST
+                if (kb >= 1) mbar_wait(&empty[sn], ((kb - 1) / NST) & 1);
+                load(sn, kn);
             }
         }
         umma_commit(done);

@@ -254,6 +254,28 @@ def test_large_ell_path_parity(orc):
     assert rel_fro(s.query_gram(0, n), ref.inner.query_gram(0, n)) < 1e-8
 
 
+def test_doubling_past_64_columns_matches_oracle(orc):
+    """simul_iter with k > 64 (sketch.cpp:108-118 doubling up to
+    kmax = min(ell, d, r); linalg.cpp:123-152): 150 Gaussian rows are
+    buffered under a huge threshold (no gate fires), then a tiny threshold
+    makes the next row's doubling run k = 2, 4, .., 64, 128, 151 = kmax = r
+    and dump xi = 151 directions at once; a small max_batch keeps the work
+    buffers at their minimum size (ncols = min(ell, d)). Trace bit-exact and
+    the restored Gram against the oracle."""
+    d, n0 = 200, 150
+    rows = np.stack([gaussian_vec(orc, d, 900 + i) for i in range(n0 + 6)])
+    ts = np.arange(1, n0 + 7)
+    th = np.concatenate([np.full(n0, 1e12), np.full(6, 1e-9)])
+    ref = orc.AeroState(d, 1 / 100, 1e12, 3, 0)
+    ev_ref = ref.update_block(rows, ts, thetas=th)
+    s = prod.AeroState(d, 1 / 100, 1e12, seed=3, stream=0, max_batch=8)
+    ev = s.update_block(rows, ts, thetas=th)
+    assert ev_ref["k_last"].max() == 151 and ev_ref["xi"].max() == 151
+    assert ev_ref["doubling_steps"].max() == 8
+    assert_trace_equal(ev, ev_ref, rtol=1e-7)
+    assert rel_fro(s.query_gram(0, n0 + 6), ref.query_gram(0, n0 + 6)) < 1e-9
+
+
 def test_grid_eigensolver_reduce_path_parity(orc):
     """ell=512 (2ell=1024 > 512): the reduce runs the persistent-grid
     tridiagonalization; two reduces inside the stream."""
