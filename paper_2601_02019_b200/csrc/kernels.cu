@@ -529,7 +529,8 @@ __device__ void small_eig(double* W, double* T, int k, double* cs) {
 // summed here in fixed order into shared memory (fuses k_product_reduce)
 template <int KM>
 __host__ __device__ constexpr size_t normalize_smem_doubles(int R, bool ws) {
-    return 32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM) + (ws ? (size_t)R * KM : 0);
+    // ws: the job's r x k product, reused as the padded staging of the new iterate (8 r8p <= r + 16 per column)
+    return 32 * 16 + 3 * KM * KM + KM + jacobi_scratch_doubles(KM) + (ws ? (size_t)(R + 16) * KM : 0);
 }
 
 // one job's normalization after product phase `phase` (body of k_iter_normalize;
@@ -832,7 +833,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
 #pragma unroll
                 for (int a = 0; a < KM; ++a) {
                     if (a < k && i < r) {
-                        xr[u][a] = x[i + (int64_t)a * ldx];
+                        xr[u][a] = last ? x[i + (int64_t)a * ldx] : 0.0;  // H = X T only in the last phase
                         yr[u][a] = y[i + (int64_t)a * ldy];
                     }
                 }
@@ -872,6 +873,10 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
             // is past the update loop), then slice 8 consecutive entries per
             // thread into one 8-byte store per slice (was one byte store per
             // slice and entry)
+            // (entry i at (i & 7) * r8p + (i >> 3), r8p odd: the 8 consecutive
+            // entries a thread slices sit r8p apart, so a warp's reads are
+            // consecutive words instead of 64-byte strides -- no bank conflicts)
+            const int r8p = ((r + 7) >> 3) | 1;
             int eb[KM];
 #pragma unroll
             for (int b = 0; b < KM; ++b) {
@@ -883,7 +888,7 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
 #pragma unroll
                 for (int u = 0; u < RU; ++u) {
                     const int i = tid + u * nt;
-                    if (i < r) ysh[i + b * r] = hv[u][b];
+                    if (i < r) ysh[(i & 7) * r8p + (i >> 3) + b * 8 * r8p] = hv[u][b];
                 }
             }
             __syncthreads();
@@ -895,7 +900,8 @@ __device__ void normalize_job(const IterJob& jb, int jidx, int phase, double* X,
                 for (int k0 = 8 * tid; k0 < r; k0 += 8 * nt) {
                     double xv[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) xv[u] = (k0 + u < r) ? ysh[k0 + u + b * r] : 0.0;
+                    for (int u = 0; u < 8; ++u)
+                        xv[u] = (k0 + u < r) ? ysh[u * r8p + (k0 >> 3) + b * 8 * r8p] : 0.0;
                     uint64_t pk[kOzSlices];
                     ozaki_slice8_pow2<kOzSlices>(xv, eb[b], pk);
                     int8_t* blk = xs.b + ((int64_t)tt * nkb + k0 / kOzBK) * kOzSlices * kOzBN * kOzBK + rr * kOzBK +
