@@ -1139,6 +1139,8 @@ int ozaki_splits(const OzakiGram& oz, int N, size_t ws_doubles) {
     }
     const int tm = oz.Rp / kOzBM, tn = (N + kOzBN - 1) / kOzBN, nkb = oz.Kp / kOzBK;
     int splits = std::max(1, std::min(sms / std::max(tm * tn, 1), nkb / 2));
+    static const int max_splits = getenv("AERO_OZ_MAXSPLIT") ? std::max(1, atoi(getenv("AERO_OZ_MAXSPLIT"))) : 1 << 20;
+    splits = std::min(splits, max_splits);  // dev knob: fewer splits = less partial traffic, fewer busy CTAs
     while (splits > 1 && (size_t)splits * (oz.R + 1) * N > ws_doubles) --splits;  // padded leading dimension
     const int per = (nkb + splits - 1) / splits;
     return (nkb + per - 1) / per;
