@@ -24,6 +24,4 @@ void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch, int6
 
 void eigh_forget(cudaStream_t st) { eigh_large_forget(st); }
 
-void eigh_release() {}
-
 }  // namespace aero_b200

@@ -143,7 +143,6 @@ constexpr int kSmallEigMax = 32;
 constexpr int kBatchedJacobiMax = 96;
 void eigh(cudaStream_t st, int n, double* A, int lda, double* w, int batch = 1,
           int64_t stride = 0, int nvec = 0);
-void eigh_release();  // free cached solver handles/workspaces
 void eigh_forget(cudaStream_t st);  // free the solver cached for one stream
 
 // columns of V (n x ncol, ld) scaled: V[:, i] *= scale[i]

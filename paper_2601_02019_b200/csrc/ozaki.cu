@@ -31,7 +31,8 @@
 // swizzle), so a pipeline stage is two bulk copies (cp.async.bulk, mbarrier
 // transaction count) issued by one thread; the same thread issues the
 // S(S+1)/2 x 2 MMAs (M128 N64 K32) of a stage into S TMEM accumulators
-// (S x 64 columns) and commits to the stage's "empty" mbarrier. Two stages.
+// (S x 64 columns) and commits to the stage's "empty" mbarrier. Three 72 KiB
+// stages at S = 6 (two bulk loads in flight behind the stage being read).
 // The eight warps then read the accumulators (tcgen05.ld; warp w: TMEM lanes
 // 32 (w % 4).., columns 32 (w / 4)..) and combine the diagonals in fp64.
 // Deterministic split-K (fixed-order sum).

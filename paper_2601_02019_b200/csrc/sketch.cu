@@ -894,7 +894,11 @@ void Sketch::process_rows(const double* dev_rows, int64_t n, const int64_t* t,
         // 192 rows 1938 ms per 40960 rows; 48: 2120, 96: 1909)
         int cap = max_batch_;
         if (i8_ && r_ + 1 >= i8_min_rows_ && persistent_ && cfg_max_batch_ == 0)
-            cap = std::min(cap, (!amp_ && fire_ema_ >= 0.5) ? 64 : 192);
+        {
+            // dev knob AERO_I8_BATCH_CAP: rows per FIRE1 batch (sweep in DESIGN.md 5)
+            static const int fire_cap = getenv("AERO_I8_BATCH_CAP") ? std::max(16, atoi(getenv("AERO_I8_BATCH_CAP"))) : 64;
+            cap = std::min(cap, (!amp_ && fire_ema_ >= 0.5) ? fire_cap : 192);
+        }
         cur_batch_ = (int)std::clamp(std::sqrt(two_alpha / p), 16.0, (double)cap);
         const int64_t B = std::min<int64_t>({(int64_t)cur_batch_, n - pos, room});
         const int64_t mp0 = mispredicts;
